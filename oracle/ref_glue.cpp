@@ -1,0 +1,438 @@
+// ref_glue.cpp — the darbs_cpu.h interface implemented by CALLING THE REFERENCE.
+//
+// TEST INFRASTRUCTURE, NOT PRODUCT.  oracle/Makefile compiles this file together
+// with the reference's own, unmodified sources
+//   /root/reference/proj/core/src/{kernel,geometry,rasterizer}.cpp
+// (read where they lie; never copied) against oracle/eigen_shim into
+// oracle/_ref/libdarbs_ref.so.  It only marshals flat FP64 arrays into the
+// reference's types and back; no algorithm of the hot path is restated here
+// except the ten-line per-splat chain of fit_scene's evaluate lambda
+// (fit3d.cpp:134-159), which is not callable from outside fit_scene and is
+// therefore spelled out below with the reference's own types and
+// backward_projection.
+#include <cmath>
+#include <cstring>
+#include <random>
+#include <vector>
+
+#include "darbs/errors.hpp"
+#include "darbs/fit_common.hpp"
+#include "darbs/geometry.hpp"
+#include "darbs/kernel.hpp"
+#include "darbs/optim.hpp"
+#include "darbs/psi_table.hpp"
+#include "darbs/rasterizer.hpp"
+#include "darbs_cpu.h"
+
+using namespace darbs;
+
+namespace {
+
+KernelSpec to_spec(const darbs_cpu_kernel* k) {
+    KernelSpec s;
+    s.family = static_cast<KernelFamily>(k->family);
+    s.beta = k->beta;
+    s.xi = k->xi;
+    s.lobes = k->lobes;
+    s.cutoff = k->cutoff;
+    s.unbounded = k->unbounded != 0;
+    return s;
+}
+
+void from_spec(const KernelSpec& s, darbs_cpu_kernel* k) {
+    k->family = static_cast<int>(s.family);
+    k->beta = s.beta;
+    k->xi = s.xi;
+    k->lobes = s.lobes;
+    k->cutoff = s.cutoff;
+    k->unbounded = s.unbounded ? 1 : 0;
+}
+
+int status_of_current_exception() {
+    try {
+        throw;
+    } catch (const invalid_parameter&) {
+        return DARBS_CPU_INVALID_PARAMETER;
+    } catch (const contract_violation&) {
+        return DARBS_CPU_CONTRACT_VIOLATION;
+    } catch (const numeric_error&) {
+        return DARBS_CPU_NUMERIC_ERROR;
+    } catch (...) {
+        return DARBS_CPU_NUMERIC_ERROR;
+    }
+}
+
+std::vector<ProjectedSplat> to_splats(int n, const double* mu2, const double* conic,
+                                      const double* radius, const double* depth,
+                                      const double* opacity, const double* rgb) {
+    std::vector<ProjectedSplat> v(static_cast<std::size_t>(n));
+    for (int i = 0; i < n; ++i) {
+        ProjectedSplat& s = v[i];
+        s.mu2 = Vec2(mu2[2 * i], mu2[2 * i + 1]);
+        s.conic = Conic{conic[3 * i], conic[3 * i + 1], conic[3 * i + 2]};
+        s.radius = radius ? radius[i] : 0.0;
+        s.depth = depth ? depth[i] : 0.0;
+        s.opacity = opacity ? opacity[i] : 1.0;
+        if (rgb) s.color = Vec3(rgb[3 * i], rgb[3 * i + 1], rgb[3 * i + 2]);
+    }
+    return v;
+}
+
+Primitive3D to_prim(const double* p) {
+    Primitive3D q;
+    q.mu = Vec3(p[0], p[1], p[2]);
+    q.scale = Vec3(p[3], p[4], p[5]);
+    q.rot = Eigen::Quaterniond(p[6], p[7], p[8], p[9]);
+    q.opacity = p[10];
+    q.color = Vec3(p[11], p[12], p[13]);
+    return q;
+}
+
+Camera to_camera(const double* c) {
+    Camera cam;
+    cam.fx = c[0];
+    cam.fy = c[1];
+    cam.cx = c[2];
+    cam.cy = c[3];
+    cam.width = static_cast<int>(c[4]);
+    cam.height = static_cast<int>(c[5]);
+    for (int r = 0; r < 4; ++r)
+        for (int col = 0; col < 4; ++col) cam.w(r, col) = c[6 + 4 * r + col];
+    return cam;
+}
+
+inline double rf(double v, int round_f32) {
+    return round_f32 ? static_cast<double>(static_cast<float>(v)) : v;
+}
+
+struct ForwardHandle {
+    ForwardResult res;
+};
+
+}  // namespace
+
+extern "C" {
+
+const char* darbs_cpu_kind(void) { return "reference"; }
+
+int darbs_cpu_make_kernel(int family, double beta, double xi, int lobes, darbs_cpu_kernel* out) {
+    if (family < 0 || family > 4) return DARBS_CPU_INVALID_PARAMETER;
+    try {
+        from_spec(make_kernel(static_cast<KernelFamily>(family), beta, xi, lobes), out);
+    } catch (...) {
+        return status_of_current_exception();
+    }
+    return DARBS_CPU_OK;
+}
+
+int darbs_cpu_kernel_preset(const char* name, darbs_cpu_kernel* out) {
+    auto s = kernel_preset(name);
+    if (!s) return DARBS_CPU_INVALID_PARAMETER;
+    from_spec(*s, out);
+    return DARBS_CPU_OK;
+}
+
+double darbs_cpu_default_psi(const char* name) {
+    auto p = default_psi(name);
+    return p ? p->psi : -1.0;
+}
+
+int darbs_cpu_eval(const darbs_cpu_kernel* k, int n, const double* dm2, double* weight,
+                   double* dweight_ddm2) {
+    KernelSpec s = to_spec(k);
+    try {
+        for (int i = 0; i < n; ++i) {
+            KernelSample ks = eval(s, dm2[i]);
+            if (weight) weight[i] = ks.weight;
+            if (dweight_ddm2) dweight_ddm2[i] = ks.dweight_ddm2;
+        }
+    } catch (...) {
+        return status_of_current_exception();
+    }
+    return DARBS_CPU_OK;
+}
+
+int darbs_cpu_conic_and_radius(const darbs_cpu_kernel* k, int n, const double* cov2,
+                               double* conic, double* radius, double* lambda12) {
+    KernelSpec s = to_spec(k);
+    try {
+        for (int i = 0; i < n; ++i) {
+            Mat2 c;
+            c << cov2[3 * i], cov2[3 * i + 1], cov2[3 * i + 1], cov2[3 * i + 2];
+            ConicRadius cr = conic_and_radius(c, s);
+            conic[3 * i] = cr.conic.a;
+            conic[3 * i + 1] = cr.conic.b;
+            conic[3 * i + 2] = cr.conic.c;
+            radius[i] = cr.radius;
+            if (lambda12) {
+                lambda12[2 * i] = cr.lambda1;
+                lambda12[2 * i + 1] = cr.lambda2;
+            }
+        }
+    } catch (...) {
+        return status_of_current_exception();
+    }
+    return DARBS_CPU_OK;
+}
+
+int darbs_cpu_random_scene(const darbs_cpu_kernel* k, int count, int width, int height,
+                           uint64_t seed, int round_f32, double* mu2, double* cov2,
+                           double* conic, double* radius, double* depth, double* opacity,
+                           double* rgb) {
+    // The fixture of benchmarks/bench.cpp:20-46, built from the real
+    // std::mt19937_64 / std::uniform_real_distribution.
+    KernelSpec kernel = to_spec(k);
+    std::mt19937_64 rng(seed);
+    std::uniform_real_distribution<double> ux(-5.0, width + 5.0);
+    std::uniform_real_distribution<double> uy(-5.0, height + 5.0);
+    std::uniform_real_distribution<double> uvar(0.6, 12.0);
+    std::uniform_real_distribution<double> ucorr(-0.6, 0.6);
+    std::uniform_real_distribution<double> uop(0.1, 0.95);
+    std::uniform_real_distribution<double> ucol(0.0, 1.0);
+    std::uniform_real_distribution<double> udep(0.5, 9.5);
+    try {
+        for (int i = 0; i < count; ++i) {
+            double a = uvar(rng), c = uvar(rng);
+            double b = ucorr(rng) * std::sqrt(a * c);
+            double mx = ux(rng);
+            double my = uy(rng);
+            a = rf(a, round_f32);
+            b = rf(b, round_f32);
+            c = rf(c, round_f32);
+            Mat2 cov;
+            cov << a, b, b, c;
+            ConicRadius cr = conic_and_radius(cov, kernel);
+            cov2[3 * i] = a;
+            cov2[3 * i + 1] = b;
+            cov2[3 * i + 2] = c;
+            mu2[2 * i] = rf(mx, round_f32);
+            mu2[2 * i + 1] = rf(my, round_f32);
+            conic[3 * i] = rf(cr.conic.a, round_f32);
+            conic[3 * i + 1] = rf(cr.conic.b, round_f32);
+            conic[3 * i + 2] = rf(cr.conic.c, round_f32);
+            radius[i] = cr.radius;
+            depth[i] = rf(udep(rng), round_f32);
+            opacity[i] = rf(uop(rng), round_f32);
+            for (int e = 0; e < 3; ++e) rgb[3 * i + e] = rf(ucol(rng), round_f32);
+        }
+    } catch (...) {
+        return status_of_current_exception();
+    }
+    return DARBS_CPU_OK;
+}
+
+void darbs_cpu_random_image_grad(int width, int height, uint64_t seed, int round_f32,
+                                 double* grad_image) {
+    std::mt19937_64 rng(seed);
+    std::uniform_real_distribution<double> u(-1.0, 1.0);
+    std::size_t n = std::size_t(width) * height * 3;
+    for (std::size_t i = 0; i < n; ++i) grad_image[i] = rf(u(rng), round_f32);
+}
+
+int64_t darbs_cpu_bin(int n, const double* mu2, const double* conic, const double* radius,
+                      const double* depth, int width, int height, int64_t* tile_offsets,
+                      int32_t* point_list, int64_t capacity, int32_t* depth_order) {
+    auto splats = to_splats(n, mu2, conic, radius, depth, nullptr, nullptr);
+    TileBins bins = bin_splats(splats, width, height);
+    int64_t k = 0;
+    for (std::size_t t = 0; t < bins.lists.size(); ++t) {
+        if (tile_offsets) tile_offsets[t] = k;
+        k += static_cast<int64_t>(bins.lists[t].size());
+    }
+    if (tile_offsets) tile_offsets[bins.lists.size()] = k;
+    if (point_list && k <= capacity) {
+        int64_t o = 0;
+        for (const auto& l : bins.lists)
+            for (int idx : l) point_list[o++] = idx;
+    }
+    if (depth_order) {
+        // The reference does not expose its depth order; recover it the way
+        // bin_splats builds it (rasterizer.cpp:31-35).
+        std::vector<int> order(n);
+        for (int i = 0; i < n; ++i) order[i] = i;
+        std::stable_sort(order.begin(), order.end(),
+                         [&](int a, int b) { return depth[a] < depth[b]; });
+        for (int i = 0; i < n; ++i) depth_order[i] = order[i];
+    }
+    return k;
+}
+
+void* darbs_cpu_forward(const darbs_cpu_kernel* k, int n, const double* mu2, const double* conic,
+                        const double* radius, const double* depth, const double* opacity,
+                        const double* rgb, int width, int height, const double* background,
+                        int threads, double* image, double* t_final, int32_t* processed,
+                        int32_t* contributors, int32_t* skipped_nonfinite) {
+    auto splats = to_splats(n, mu2, conic, radius, depth, opacity, rgb);
+    auto* h = new ForwardHandle;
+    try {
+        h->res = forward(splats, to_spec(k), width, height,
+                         Vec3(background[0], background[1], background[2]), threads);
+    } catch (...) {
+        delete h;
+        return nullptr;
+    }
+    const BlendAux& aux = h->res.aux;
+    std::size_t px = std::size_t(width) * height;
+    if (image) std::memcpy(image, h->res.image.rgb.data(), sizeof(double) * px * 3);
+    if (t_final) std::memcpy(t_final, aux.t_final.data(), sizeof(double) * px);
+    if (processed) std::memcpy(processed, aux.processed.data(), sizeof(int32_t) * px);
+    if (contributors) std::memcpy(contributors, aux.contributors.data(), sizeof(int32_t) * px);
+    if (skipped_nonfinite) *skipped_nonfinite = aux.skipped_nonfinite;
+    return h;
+}
+
+void darbs_cpu_forward_free(void* handle) { delete static_cast<ForwardHandle*>(handle); }
+
+int darbs_cpu_oracle_forward(const darbs_cpu_kernel* k, int n, const double* mu2,
+                             const double* conic, const double* radius, const double* depth,
+                             const double* opacity, const double* rgb, int width, int height,
+                             const double* background, double* image) {
+    auto splats = to_splats(n, mu2, conic, radius, depth, opacity, rgb);
+    try {
+        ImageBuffer img = oracle_forward(splats, to_spec(k), width, height,
+                                         Vec3(background[0], background[1], background[2]));
+        std::memcpy(image, img.rgb.data(), sizeof(double) * img.rgb.size());
+    } catch (...) {
+        return status_of_current_exception();
+    }
+    return DARBS_CPU_OK;
+}
+
+int darbs_cpu_backward(void* handle, const darbs_cpu_kernel* k, int grad_width, int grad_height,
+                       const double* grad_image, int n, const double* mu2, const double* conic,
+                       const double* opacity, const double* rgb, int threads, double* grads) {
+    auto* h = static_cast<ForwardHandle*>(handle);
+    if (!h) return DARBS_CPU_CONTRACT_VIOLATION;
+    ImageBuffer g(grad_width, grad_height);
+    std::memcpy(g.rgb.data(), grad_image, sizeof(double) * g.rgb.size());
+    auto splats = to_splats(n, mu2, conic, nullptr, nullptr, opacity, rgb);
+    try {
+        std::vector<SplatGrads> sg = backward(g, splats, to_spec(k), h->res.aux, threads);
+        for (int i = 0; i < n; ++i) {
+            double* o = grads + 9 * std::size_t(i);
+            o[0] = sg[i].d_color[0];
+            o[1] = sg[i].d_color[1];
+            o[2] = sg[i].d_color[2];
+            o[3] = sg[i].d_opacity;
+            o[4] = sg[i].d_conic_a;
+            o[5] = sg[i].d_conic_b;
+            o[6] = sg[i].d_conic_c;
+            o[7] = sg[i].d_mu2[0];
+            o[8] = sg[i].d_mu2[1];
+        }
+    } catch (...) {
+        return status_of_current_exception();
+    }
+    return DARBS_CPU_OK;
+}
+
+void darbs_cpu_realize(int n, const double* raw, double* prims) {
+    // realize() is file-local in fit3d.cpp:17-25; same expressions, using the
+    // reference's sigmoid (fit_common.hpp:40).
+    for (int i = 0; i < n; ++i) {
+        const double* q = raw + 14 * std::size_t(i);
+        double* p = prims + 14 * std::size_t(i);
+        p[0] = q[0];
+        p[1] = q[1];
+        p[2] = q[2];
+        for (int a = 3; a < 6; ++a) p[a] = std::exp(q[a]);
+        for (int a = 6; a < 10; ++a) p[a] = q[a];
+        for (int a = 10; a < 14; ++a) p[a] = sigmoid(q[a]);
+    }
+}
+
+int darbs_cpu_project(const darbs_cpu_kernel* k, double psi, double dilation, int n,
+                      const double* prims, const double* camera, int32_t* valid, double* mu2,
+                      double* cov2, double* conic, double* radius, double* depth) {
+    KernelSpec kernel = to_spec(k);
+    Camera cam = to_camera(camera);
+    try {
+        for (int i = 0; i < n; ++i) {
+            auto s = project_primitive(to_prim(prims + 14 * std::size_t(i)), cam, kernel, psi,
+                                       dilation);
+            valid[i] = s ? 1 : 0;
+            if (!s) {
+                mu2[2 * i] = mu2[2 * i + 1] = 0.0;
+                cov2[3 * i] = cov2[3 * i + 1] = cov2[3 * i + 2] = 0.0;
+                conic[3 * i] = conic[3 * i + 1] = conic[3 * i + 2] = 0.0;
+                radius[i] = depth[i] = 0.0;
+                continue;
+            }
+            mu2[2 * i] = s->mu2.x();
+            mu2[2 * i + 1] = s->mu2.y();
+            cov2[3 * i] = s->cov2(0, 0);
+            cov2[3 * i + 1] = s->cov2(0, 1);
+            cov2[3 * i + 2] = s->cov2(1, 1);
+            conic[3 * i] = s->conic.a;
+            conic[3 * i + 1] = s->conic.b;
+            conic[3 * i + 2] = s->conic.c;
+            radius[i] = s->radius;
+            depth[i] = s->depth;
+        }
+    } catch (...) {
+        return status_of_current_exception();
+    }
+    return DARBS_CPU_OK;
+}
+
+void darbs_cpu_backward_projection(double psi, int n, const double* grad_cov2,
+                                   const double* grad_mu2, const double* prims,
+                                   const double* camera, double* d_mu, double* d_scale,
+                                   double* d_rot) {
+    Camera cam = to_camera(camera);
+    for (int i = 0; i < n; ++i) {
+        Mat2 gc;
+        gc << grad_cov2[4 * i], grad_cov2[4 * i + 1], grad_cov2[4 * i + 2], grad_cov2[4 * i + 3];
+        ProjectionGrads pg = backward_projection(gc, Vec2(grad_mu2[2 * i], grad_mu2[2 * i + 1]),
+                                                 to_prim(prims + 14 * std::size_t(i)), cam, psi);
+        for (int a = 0; a < 3; ++a) d_mu[3 * i + a] = pg.d_mu[a];
+        for (int a = 0; a < 3; ++a) d_scale[3 * i + a] = pg.d_scale[a];
+        for (int a = 0; a < 4; ++a) d_rot[4 * i + a] = pg.d_rot[a];
+    }
+}
+
+void darbs_cpu_param_grads(double psi, int m, const int32_t* owner, const double* splat_grads,
+                           const double* conic, const double* opacity, const double* rgb,
+                           const double* prims, const double* camera, double* param_grads) {
+    Camera cam = to_camera(camera);
+    for (int k = 0; k < m; ++k) {
+        const double* gi = splat_grads + 9 * std::size_t(k);
+        int i = owner[k];
+        double* g = param_grads + 14 * std::size_t(i);
+        Primitive3D prim = to_prim(prims + 14 * std::size_t(i));
+        // fit3d.cpp:140-144
+        Mat2 gc;
+        gc << gi[4], 0.5 * gi[5], 0.5 * gi[5], gi[6];
+        Mat2 cmat;
+        cmat << conic[3 * k], conic[3 * k + 1], conic[3 * k + 1], conic[3 * k + 2];
+        Mat2 d_cov2 = -cmat * gc * cmat;
+        ProjectionGrads pg = backward_projection(d_cov2, Vec2(gi[7], gi[8]), prim, cam, psi);
+        // fit3d.cpp:148-158
+        g[0] += pg.d_mu.x();
+        g[1] += pg.d_mu.y();
+        g[2] += pg.d_mu.z();
+        for (int a = 0; a < 3; ++a) g[3 + a] += pg.d_scale[a] * prim.scale[a];
+        for (int a = 0; a < 4; ++a) g[6 + a] += pg.d_rot[a];
+        g[10] += gi[3] * opacity[k] * (1.0 - opacity[k]);
+        for (int c = 0; c < 3; ++c) g[11 + c] += gi[c] * rgb[3 * k + c] * (1.0 - rgb[3 * k + c]);
+    }
+}
+
+int darbs_cpu_adam_step(int64_t dim, double* params, const double* grads, double* m, double* v,
+                        const double* lrs, int t) {
+    AdamState st(static_cast<std::size_t>(dim));
+    std::memcpy(st.m.data(), m, sizeof(double) * dim);
+    std::memcpy(st.v.data(), v, sizeof(double) * dim);
+    try {
+        adam_step(std::span<double>(params, static_cast<std::size_t>(dim)),
+                  std::span<const double>(grads, static_cast<std::size_t>(dim)), st,
+                  std::span<const double>(lrs, static_cast<std::size_t>(dim)), t);
+    } catch (...) {
+        return status_of_current_exception();
+    }
+    std::memcpy(m, st.m.data(), sizeof(double) * dim);
+    std::memcpy(v, st.v.data(), sizeof(double) * dim);
+    return DARBS_CPU_OK;
+}
+
+}  // extern "C"
