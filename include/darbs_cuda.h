@@ -1,0 +1,247 @@
+/*
+ * darbs_cuda.h — C ABI of the B200-native DARBF splatting rasterizer.
+ *
+ * This is the drop-in boundary for the reference's rasterizer hot path
+ * (arxiv/paper_2501_12369, proj/core).  The reference has no FFI of its own:
+ * its interface for this path is a handful of C++ free functions in namespace
+ * darbs.  Each entry point below names the reference interface it replaces
+ * (paths relative to the reference's proj/core/).  The C++ mirror of those
+ * functions, with the reference's own signatures, lives in
+ * paper_2501_12369_b200/host/darbs_b200.hpp and only calls this ABI.
+ *
+ * Conventions
+ *  - plain pointers and sizes; no C++ or torch types.
+ *  - every array argument of one call lives in ONE memory space, named by the
+ *    `space` argument: DARBS_HOST (the library stages through its own device
+ *    workspace and copies results back before returning) or DARBS_DEVICE
+ *    (pointers are device pointers on the context's GPU; the call is
+ *    asynchronous on the context's stream unless stated otherwise).
+ *  - element type is float32 on the wire (the reference is float64; see
+ *    DESIGN.md "precision policy").  Images are row-major, RGB interleaved
+ *    (include/darbs/image.hpp:9-20).  Splats are structure-of-arrays.
+ *  - every function returns a darbs_status; the reference's exceptions map to
+ *    status codes as listed at the enum.  darbs_cuda_last_error() gives the
+ *    message of the last failure on the context.
+ *  - a context belongs to one host thread and one GPU; calls on it are
+ *    serialised on its stream.
+ *  - there is no CPU fallback: if no CUDA device is usable, create fails.
+ */
+#ifndef DARBS_CUDA_H
+#define DARBS_CUDA_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#if defined(_WIN32)
+#define DARBS_API
+#else
+#define DARBS_API __attribute__((visibility("default")))
+#endif
+
+/* include/darbs/errors.hpp:10-36 and the CLI's exit-code mapping tools/main.cpp:487-499 */
+typedef enum {
+    DARBS_OK = 0,
+    DARBS_INVALID_PARAMETER = 1,  /* darbs::invalid_parameter */
+    DARBS_NUMERIC_ERROR = 2,      /* darbs::numeric_error, darbs::degenerate_covariance */
+    DARBS_IO_ERROR = 3,           /* darbs::io_error (unused on this path) */
+    DARBS_CONTRACT_VIOLATION = 4, /* darbs::contract_violation */
+    DARBS_CUDA_ERROR = 5          /* CUDA runtime failure (no reference analogue) */
+} darbs_status;
+
+typedef enum { DARBS_HOST = 0, DARBS_DEVICE = 1 } darbs_space;
+
+/* include/darbs/kernel.hpp:12-18 */
+typedef enum {
+    DARBS_GAUSSIAN = 0,
+    DARBS_HALF_COSINE = 1,
+    DARBS_RAISED_COSINE = 2,
+    DARBS_MODULUS_SINC = 3,
+    DARBS_INVERSE_MULTIQUADRATIC = 4
+} darbs_family;
+
+/* KernelSpec, include/darbs/kernel.hpp:20-33 */
+typedef struct {
+    int32_t family;
+    double beta;
+    double xi;
+    int32_t lobes;
+    double cutoff;
+    int32_t unbounded;
+} darbs_kernel_spec;
+
+/* rasterizer constants, include/darbs/rasterizer.hpp:11-14 */
+#define DARBS_TILE_SIZE 16
+#define DARBS_ALPHA_CLAMP 0.99
+#define DARBS_ALPHA_SKIP (1.0 / 255.0)
+#define DARBS_TRANSMITTANCE_FLOOR 1e-4
+/* include/darbs/geometry.hpp:55-56 */
+#define DARBS_NEAR_PLANE 0.01
+#define DARBS_DILATION 0.3
+/* fit3d.cpp:15 — mu(3) log_scale(3) quat wxyz(4) logit_opacity logit_rgb(3) */
+#define DARBS_PARAMS_PER_PRIMITIVE 14
+/* SplatGrads, include/darbs/rasterizer.hpp:53-60: d_color[3] d_opacity d_conic_a d_conic_b d_conic_c d_mu2[2] */
+#define DARBS_GRADS_PER_SPLAT 9
+/* camera block, include/darbs/scene_io.hpp:16-19: fx fy cx cy width height + 16 row-major world-to-camera */
+#define DARBS_CAMERA_DOUBLES 22
+
+typedef struct darbs_cuda_ctx darbs_cuda_ctx;
+
+/* ---- library / context ---------------------------------------------------- */
+
+DARBS_API const char* darbs_cuda_version(void);
+
+/* Creates a context on CUDA device `device` with its own non-blocking stream. */
+DARBS_API darbs_status darbs_cuda_create(int device, darbs_cuda_ctx** out_ctx);
+DARBS_API void darbs_cuda_destroy(darbs_cuda_ctx* ctx);
+/* Message of the last non-OK status on this context ("" if none); ctx may be
+ * NULL for create failures. */
+DARBS_API const char* darbs_cuda_last_error(const darbs_cuda_ctx* ctx);
+/* Use an externally owned cudaStream_t (e.g. torch's current stream) for all
+ * subsequent work; NULL restores the context's own stream. */
+DARBS_API darbs_status darbs_cuda_set_stream(darbs_cuda_ctx* ctx, void* cuda_stream);
+DARBS_API darbs_status darbs_cuda_synchronize(darbs_cuda_ctx* ctx);
+/* Number of kernels this library has launched on the context since creation
+ * (its own kernels and the CUB primitives it calls). */
+DARBS_API int64_t darbs_cuda_launch_count(const darbs_cuda_ctx* ctx);
+/* 1: decisions that fall inside the FP32 guard band of a threshold are re-taken
+ * in FP64 exactly as the reference takes them (default).  0: pure FP32. */
+DARBS_API darbs_status darbs_cuda_set_exact_decisions(darbs_cuda_ctx* ctx, int enabled);
+
+/* ---- kernel family ---------------------------------------------------------- */
+
+/* make_kernel, src/kernel.cpp:42-65 (host-side; validates and fills cutoff). */
+DARBS_API darbs_status darbs_cuda_make_kernel(int family, double beta, double xi, int lobes,
+                                              darbs_kernel_spec* out);
+/* kernel_preset, src/kernel.cpp:223-240: "gaussian", "half-cosine-sq",
+ * "raised-cosine", "mod-sinc", "inv-multiquadratic". */
+DARBS_API darbs_status darbs_cuda_kernel_preset(const char* name, darbs_kernel_spec* out);
+/* default_psi, include/darbs/psi_table.hpp:20-32; negative when unknown. */
+DARBS_API double darbs_cuda_default_psi(const char* name);
+/* eval, src/kernel.cpp:127-164, on the device functors the render kernels use
+ * (FP32 fast path; `exact` != 0 evaluates the FP64 path instead). */
+DARBS_API darbs_status darbs_cuda_eval(darbs_cuda_ctx* ctx, const darbs_kernel_spec* kernel,
+                                       int64_t n, const float* dm2, float* weight,
+                                       float* dweight_ddm2, int exact, darbs_space space);
+
+/* ---- rasterizer ------------------------------------------------------------- */
+
+/* bin_splats, src/rasterizer.cpp:25-53 (TileBins, include/darbs/rasterizer.hpp:16-20).
+ * Outputs (each may be NULL): num_entries (host int64, always host);
+ * tile_ranges [2*tiles] = (begin, end) into point_list per tile, row-major tiles;
+ * point_list [K] = splat indices, depth-ascending per tile, ties by index;
+ * sort_keys  [K] = (tile_id << 32) | depth-order rank of the entry's splat;
+ * depth_order[n] = splat indices in stable depth order.  `capacity` bounds the
+ * K-sized outputs; if K > capacity they are not written and the call still
+ * returns DARBS_OK with *num_entries = K. */
+DARBS_API darbs_status darbs_cuda_bin(darbs_cuda_ctx* ctx, int64_t n, const float* mu2,
+                                      const float* conic, const float* radius, const float* depth,
+                                      int width, int height, int64_t* num_entries,
+                                      int32_t* tile_ranges, int32_t* point_list,
+                                      uint64_t* sort_keys, int32_t* depth_order, int64_t capacity,
+                                      darbs_space space);
+
+/* forward, src/rasterizer.cpp:55-112 (ForwardResult / BlendAux,
+ * include/darbs/rasterizer.hpp:27-46).  mu2[2n], conic[3n] (a,b,c), radius[n],
+ * depth[n], opacity[n], rgb[3n].  Outputs (each may be NULL): image[3*w*h],
+ * t_final[w*h], processed[w*h], contributors[w*h], skipped_nonfinite (host int).
+ * The bins and per-pixel aux stay resident in the context for the matching
+ * darbs_cuda_backward, replacing the BlendAux value the reference hands back.
+ * `threads` of the reference signature has no meaning here and is omitted. */
+DARBS_API darbs_status darbs_cuda_forward(darbs_cuda_ctx* ctx, const darbs_kernel_spec* kernel,
+                                          int64_t n, const float* mu2, const float* conic,
+                                          const float* radius, const float* depth,
+                                          const float* opacity, const float* rgb, int width,
+                                          int height, const float background[3], float* image,
+                                          float* t_final, int32_t* processed,
+                                          int32_t* contributors, int32_t* skipped_nonfinite,
+                                          darbs_space space);
+
+/* backward, src/rasterizer.cpp:147-234.  grads[9n] in SplatGrads order.  Returns
+ * DARBS_CONTRACT_VIOLATION when (grad_width, grad_height, n) do not match the
+ * last forward on this context (rasterizer.cpp:151-154).  The splat arrays are
+ * re-read (the reference recomputes from the splats it is handed); pass all
+ * four as NULL to reuse the forward call's values. */
+DARBS_API darbs_status darbs_cuda_backward(darbs_cuda_ctx* ctx, const darbs_kernel_spec* kernel,
+                                           int grad_width, int grad_height,
+                                           const float* grad_image, int64_t n, const float* mu2,
+                                           const float* conic, const float* opacity,
+                                           const float* rgb, float* grads, darbs_space space);
+
+/* ---- geometry (per-primitive preprocess) ---------------------------------- */
+
+/* realize, src/fit3d.cpp:17-25: raw[14n] -> prims[14n] (mu, scale, quat wxyz, opacity, rgb). */
+DARBS_API darbs_status darbs_cuda_realize(darbs_cuda_ctx* ctx, int64_t n, const float* raw,
+                                          float* prims, darbs_space space);
+
+/* project_primitive, src/geometry.cpp:66-87, for n realized primitives.
+ * camera: 22 doubles, always host.  valid[i] = 0 when near-plane culled.
+ * cov2[3n] = (xx, xy, yy).  Status: INVALID_PARAMETER (scale <= 0, psi <= 0),
+ * NUMERIC_ERROR (covariance not positive definite), as the reference throws. */
+DARBS_API darbs_status darbs_cuda_project(darbs_cuda_ctx* ctx, const darbs_kernel_spec* kernel,
+                                          double psi, double dilation, int64_t n,
+                                          const float* prims, const double* camera,
+                                          int32_t* valid, float* mu2, float* cov2, float* conic,
+                                          float* radius, float* depth, darbs_space space);
+
+/* backward_projection, src/geometry.cpp:111-168. grad_cov2[4n] = (xx,xy,yx,yy),
+ * grad_mu2[2n]; outputs d_mu[3n], d_scale[3n], d_rot[4n] (w,x,y,z). */
+DARBS_API darbs_status darbs_cuda_backward_projection(darbs_cuda_ctx* ctx, double psi, int64_t n,
+                                                      const float* grad_cov2,
+                                                      const float* grad_mu2, const float* prims,
+                                                      const double* camera, float* d_mu,
+                                                      float* d_scale, float* d_rot,
+                                                      darbs_space space);
+
+/* ---- training step (fit_scene's evaluate + adam_step) ----------------------- */
+
+/* One view of fit_scene's evaluate lambda, src/fit3d.cpp:108-159:
+ *   realize -> project_primitive (near-plane cull) -> forward -> loss ->
+ *   backward -> conic-grad -> cov2-grad -> backward_projection ->
+ *   reparametrisation -> param_grads[14n] += .
+ * raw_params[14n] and param_grads[14n] follow `space`.  Exactly one of
+ * `target` / `grad_image` is non-NULL:
+ *   target     [3wh]: loss_total(image, target, lambda) (src/loss.cpp:173-230)
+ *                     drives the backward; *loss_out receives total, l1, dssim, mse.
+ *   grad_image [3wh]: used as dL/dimage directly (loss_out gets zeros).
+ * Only lambda == 0 (pure L1) is implemented in this round; other values return
+ * DARBS_INVALID_PARAMETER.  image_out (may be NULL) receives the rendered view.
+ * background: fit_scene uses (0,0,0) (fit3d.cpp:52).
+ * Returns NUMERIC_ERROR when every primitive is culled (fit3d.cpp:117-119) or
+ * the loss is not finite (fit3d.cpp:123-125); those checks synchronise. */
+DARBS_API darbs_status darbs_cuda_evaluate_view(darbs_cuda_ctx* ctx,
+                                                const darbs_kernel_spec* kernel, double psi,
+                                                int64_t n, const float* raw_params,
+                                                const double* camera, const float background[3],
+                                                const float* target, double lambda,
+                                                const float* grad_image, float* param_grads,
+                                                float* image_out, double loss_out[4],
+                                                darbs_space space);
+
+/* adam_step, include/darbs/optim.hpp:24-39 (beta1 .9, beta2 .999, eps 1e-15,
+ * per-parameter learning rates, t is 1-based). */
+DARBS_API darbs_status darbs_cuda_adam_step(darbs_cuda_ctx* ctx, int64_t dim, float* params,
+                                            const float* grads, float* m, float* v,
+                                            const float* lrs, int t, darbs_space space);
+
+/* ---- instrumentation ---------------------------------------------------------- */
+
+/* Device time in milliseconds of the stages of the last forward / backward /
+ * evaluate_view on this context, measured with CUDA events on the context's
+ * stream (synchronises).  out[0..7] = preprocess, binning, render_fwd, loss,
+ * render_bwd, preprocess_bwd, adam, reserved.  Recording is off by default. */
+DARBS_API darbs_status darbs_cuda_set_stage_timing(darbs_cuda_ctx* ctx, int enabled);
+DARBS_API darbs_status darbs_cuda_stage_times(darbs_cuda_ctx* ctx, double out_ms[8]);
+/* Work counters of the last forward: out[0] = K tile entries, out[1] = sum of
+ * processed (visits), out[2] = sum of contributors, out[3] = (warp, entry)
+ * pairs that survived the block-level cull, out[4] = FP64 guard-band
+ * re-decisions, out[5] = pixels flagged near the transmittance floor.
+ * Synchronises. */
+DARBS_API darbs_status darbs_cuda_work_counters(darbs_cuda_ctx* ctx, int64_t out[8]);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DARBS_CUDA_H */

@@ -1,0 +1,288 @@
+// binning.cu — device restatement of darbs::bin_splats (reference
+// src/rasterizer.cpp:25-53): global stable depth order, per-splat inclusive tile
+// rectangle, per-tile depth-ordered index lists.
+//
+// Two-level sort instead of one wide (tile, depth) key:
+//   1. stable LSD radix sort of the N (depth bits, index) pairs  -> depth order
+//      (stability gives the reference's index tie-break, rasterizer.cpp:33);
+//   2. tiles touched per splat, scanned IN DEPTH ORDER -> write offsets;
+//   3. every splat emits its (tile id, index) pairs at its offset, so the K
+//      entries are already depth-ordered globally;
+//   4. stable radix sort of the K entries on the tile id bits only
+//      (13 bits at 1080p: two 7-bit... passes) keeps depth order inside a tile;
+//   5. tile ranges from the sorted tile ids.
+// The tile rectangle is evaluated in FP64 on the float32 inputs so that
+// floor((mu -+ R)/16) is decided on exactly the values the FP64 reference sees
+// (rasterizer.cpp:40-45).
+#include <cub/cub.cuh>
+
+#include "common.cuh"
+
+namespace darbs_b200 {
+
+namespace {
+
+struct Scalars {  // lives behind the 8 work counters in ctx->counters
+    unsigned long long total_entries;
+    unsigned long long skipped_nonfinite;
+};
+
+__device__ __forceinline__ unsigned depth_to_key(float d) {
+    // order-preserving map float -> uint (negative depths included)
+    unsigned u = __float_as_uint(d);
+    return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+
+// rect packed as x0 | y0<<16 and x1 | y1<<16 ; touched == 0 -> no tiles
+__global__ void rect_kernel(int64_t n, const float* __restrict__ mu2,
+                            const float* __restrict__ conic, const float* __restrict__ radius,
+                            const float* __restrict__ depth, const int* __restrict__ valid,
+                            int tiles_x, int tiles_y, uint2* __restrict__ rects,
+                            unsigned* __restrict__ touched, unsigned* __restrict__ depth_keys,
+                            unsigned* __restrict__ order, Scalars* __restrict__ scalars) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    depth_keys[i] = depth_to_key(depth[i]);
+    order[i] = (unsigned)i;
+    bool ok = valid ? valid[i] != 0 : true;
+    unsigned cnt = 0;
+    uint2 rect = make_uint2(0, 0);
+    if (ok) {
+        float a = conic[3 * i], b = conic[3 * i + 1], c = conic[3 * i + 2], r = radius[i];
+        if (!(isfinite(a) && isfinite(b) && isfinite(c) && isfinite(r))) {  // rasterizer.cpp:39
+            atomicAdd(&scalars->skipped_nonfinite, 1ull);
+        } else {
+            double mx = mu2[2 * i], my = mu2[2 * i + 1], rd = r;
+            // rasterizer.cpp:40-45 (the clamp happens in floating point here so
+            // that huge coordinates cannot overflow the int conversion)
+            double fx0 = floor((mx - rd) / DARBS_TILE_SIZE), fy0 = floor((my - rd) / DARBS_TILE_SIZE);
+            double fx1 = floor((mx + rd) / DARBS_TILE_SIZE), fy1 = floor((my + rd) / DARBS_TILE_SIZE);
+            // NaN centres compare false everywhere -> empty rect, like an
+            // int-converted NaN would be garbage in the reference (unsupported).
+            if (fx1 >= 0.0 && fy1 >= 0.0 && fx0 <= tiles_x - 1 && fy0 <= tiles_y - 1) {
+                int x0 = (int)fmax(fx0, 0.0), y0 = (int)fmax(fy0, 0.0);
+                int x1 = (int)fmin(fx1, (double)(tiles_x - 1)), y1 = (int)fmin(fy1, (double)(tiles_y - 1));
+                if (x1 >= x0 && y1 >= y0) {
+                    cnt = (unsigned)(x1 - x0 + 1) * (unsigned)(y1 - y0 + 1);
+                    rect = make_uint2((unsigned)x0 | ((unsigned)y0 << 16),
+                                      (unsigned)x1 | ((unsigned)y1 << 16));
+                }
+            }
+        }
+    }
+    rects[i] = rect;
+    touched[i] = cnt;
+}
+
+// touched[] gathered through the depth order, so the scan runs in depth order.
+__global__ void gather_touched_kernel(int64_t n, const unsigned* __restrict__ touched,
+                                      const unsigned* __restrict__ order,
+                                      unsigned* __restrict__ touched_in_order) {
+    int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (r < n) touched_in_order[r] = touched[order[r]];
+}
+
+__global__ void total_kernel(int64_t n, const unsigned* __restrict__ offsets,
+                             const unsigned* __restrict__ touched_in_order,
+                             Scalars* __restrict__ scalars) {
+    scalars->total_entries = (unsigned long long)offsets[n - 1] + touched_in_order[n - 1];
+}
+
+__global__ void duplicate_kernel(int64_t n, const unsigned* __restrict__ order,
+                                 const unsigned* __restrict__ offsets,
+                                 const uint2* __restrict__ rects,
+                                 const unsigned* __restrict__ touched, int tiles_x,
+                                 unsigned* __restrict__ tile_keys, unsigned* __restrict__ tile_vals) {
+    int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (r >= n) return;
+    unsigned idx = order[r];
+    uint2 rect = rects[idx];
+    int x0 = rect.x & 0xffff, y0 = rect.x >> 16, x1 = rect.y & 0xffff, y1 = rect.y >> 16;
+    unsigned off = offsets[r];
+    if (touched[idx] == 0) return;  // empty rect is stored as (0,0)-(0,0)
+    for (int ty = y0; ty <= y1; ++ty)
+        for (int tx = x0; tx <= x1; ++tx) {  // rasterizer.cpp:46-50
+            tile_keys[off] = (unsigned)(ty * tiles_x + tx);
+            tile_vals[off] = idx;
+            ++off;
+        }
+}
+
+__global__ void ranges_kernel(int64_t k, const unsigned* __restrict__ sorted_tiles,
+                              int2* __restrict__ ranges) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= k) return;
+    unsigned t = sorted_tiles[i];
+    if (i == 0 || sorted_tiles[i - 1] != t) ranges[t].x = (int)i;
+    if (i == k - 1 || sorted_tiles[i + 1] != t) ranges[t].y = (int)(i + 1);
+}
+
+__global__ void export_keys_kernel(int64_t k, const unsigned* __restrict__ sorted_tiles,
+                                   const unsigned* __restrict__ point_list,
+                                   const unsigned* __restrict__ rank_of,
+                                   unsigned long long* __restrict__ keys) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= k) return;
+    keys[i] = ((unsigned long long)sorted_tiles[i] << 32) | rank_of[point_list[i]];
+}
+
+__global__ void invert_order_kernel(int64_t n, const unsigned* __restrict__ order,
+                                    unsigned* __restrict__ rank_of) {
+    int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (r < n) rank_of[order[r]] = (unsigned)r;
+}
+
+inline unsigned grid_for(int64_t n, int threads) { return (unsigned)((n + threads - 1) / threads); }
+
+int bits_for(int tiles) {
+    int b = 1;
+    while ((1 << b) < tiles) ++b;
+    return b;
+}
+
+}  // namespace
+
+const int32_t* point_list_ptr(const darbs_cuda_ctx* ctx) {
+    return (const int32_t*)ctx->tile_vals.ptr + (size_t)ctx->cur_key_buf * (ctx->tile_vals.bytes / 8);
+}
+const uint32_t* depth_order_ptr(const darbs_cuda_ctx* ctx) {
+    return (const uint32_t*)ctx->order.ptr + (size_t)ctx->cur_order_buf * (ctx->order.bytes / 8);
+}
+
+darbs_status run_binning(darbs_cuda_ctx* ctx, int64_t n, const float* mu2, const float* conic,
+                         const float* radius, const float* depth, const int32_t* valid,
+                         int width, int height) {
+    cudaStream_t s = ctx->stream;
+    ctx->tiles_x = (width + DARBS_TILE_SIZE - 1) / DARBS_TILE_SIZE;
+    ctx->tiles_y = (height + DARBS_TILE_SIZE - 1) / DARBS_TILE_SIZE;
+    const int tiles = ctx->tiles_x * ctx->tiles_y;
+    if (ctx->tiles_x > 65535 || ctx->tiles_y > 65535)
+        return fail(ctx, DARBS_INVALID_PARAMETER, "image too large for 16-bit tile coordinates");
+    if (n >= (int64_t)1 << 31) return fail(ctx, DARBS_INVALID_PARAMETER, "too many splats");
+
+    DARBS_TRY(reserve(ctx, ctx->ranges, sizeof(int2) * (size_t)(tiles > 0 ? tiles : 1)));
+    DARBS_CUDA_TRY(ctx, cudaMemsetAsync(ctx->ranges.ptr, 0, sizeof(int2) * (size_t)tiles, s));
+    Scalars* scalars = (Scalars*)((unsigned long long*)ctx->counters.ptr + 8);
+    DARBS_CUDA_TRY(ctx, cudaMemsetAsync(ctx->counters.ptr, 0, sizeof(unsigned long long) * 10, s));
+    ctx->fwd_entries = 0;
+    ctx->cur_key_buf = 0;
+    ctx->cur_order_buf = 0;
+    if (n == 0 || tiles == 0) return DARBS_OK;
+
+    const size_t nn = (size_t)n;
+    DARBS_TRY(reserve(ctx, ctx->rects, sizeof(uint2) * nn + sizeof(unsigned) * nn));
+    DARBS_TRY(reserve(ctx, ctx->depth_keys, sizeof(unsigned) * 2 * nn));
+    DARBS_TRY(reserve(ctx, ctx->order, sizeof(unsigned) * 2 * nn));
+    DARBS_TRY(reserve(ctx, ctx->offsets, sizeof(unsigned) * (nn + 1)));
+    uint2* rects = (uint2*)ctx->rects.ptr;
+    unsigned* touched = (unsigned*)(rects + nn);
+    // double buffers are split at half of the RESERVED size so that the halves
+    // stay put when the buffer is larger than this call needs.
+    unsigned* dk0 = (unsigned*)ctx->depth_keys.ptr;
+    unsigned* dk1 = dk0 + ctx->depth_keys.bytes / 8;
+    unsigned* or0 = (unsigned*)ctx->order.ptr;
+    unsigned* or1 = or0 + ctx->order.bytes / 8;
+    unsigned* offsets = (unsigned*)ctx->offsets.ptr;
+
+    rect_kernel<<<grid_for(n, 256), 256, 0, s>>>(n, mu2, conic, radius, depth, valid, ctx->tiles_x,
+                                                 ctx->tiles_y, rects, touched, dk0, or0, scalars);
+    DARBS_TRY(check_launch(ctx, "rect_kernel"));
+
+    // 1. stable depth sort
+    cub::DoubleBuffer<unsigned> dkeys(dk0, dk1);
+    cub::DoubleBuffer<unsigned> dvals(or0, or1);
+    size_t temp_bytes = 0;
+    DARBS_CUDA_TRY(ctx, cub::DeviceRadixSort::SortPairs(nullptr, temp_bytes, dkeys, dvals, (int)n, 0,
+                                                       32, s));
+    size_t scan_bytes = 0;
+    DARBS_CUDA_TRY(ctx, cub::DeviceScan::ExclusiveSum(nullptr, scan_bytes, offsets, offsets, (int)n, s));
+    DARBS_TRY(reserve(ctx, ctx->cub_temp, temp_bytes > scan_bytes ? temp_bytes : scan_bytes));
+    temp_bytes = ctx->cub_temp.bytes;
+    DARBS_CUDA_TRY(ctx, cub::DeviceRadixSort::SortPairs(ctx->cub_temp.ptr, temp_bytes, dkeys, dvals,
+                                                       (int)n, 0, 32, s));
+    ctx->launches += 5;  // onesweep: histogram + 4 digit passes
+    const unsigned* order = dvals.Current();
+    ctx->cur_order_buf = order == or0 ? 0 : 1;
+
+    // 2. offsets in depth order, total K
+    // the inactive half of the depth-key double buffer holds touched-in-depth-order
+    unsigned* touched_in_order = dkeys.Current() == dk0 ? dk1 : dk0;
+    gather_touched_kernel<<<grid_for(n, 256), 256, 0, s>>>(n, touched, order, touched_in_order);
+    DARBS_TRY(check_launch(ctx, "gather_touched_kernel"));
+    scan_bytes = ctx->cub_temp.bytes;
+    DARBS_CUDA_TRY(ctx, cub::DeviceScan::ExclusiveSum(ctx->cub_temp.ptr, scan_bytes, touched_in_order,
+                                                     offsets, (int)n, s));
+    ctx->launches += 2;
+    total_kernel<<<1, 1, 0, s>>>(n, offsets, touched_in_order, scalars);
+    DARBS_TRY(check_launch(ctx, "total_kernel"));
+    DARBS_TRY(reserve_pinned(ctx, 64));
+    DARBS_CUDA_TRY(ctx, cudaMemcpyAsync(ctx->pinned, scalars, sizeof(Scalars), cudaMemcpyDeviceToHost, s));
+    DARBS_CUDA_TRY(ctx, cudaStreamSynchronize(s));
+    const unsigned long long k = ((Scalars*)ctx->pinned)->total_entries;
+    if (k >= (1ull << 31)) return fail(ctx, DARBS_INVALID_PARAMETER, "more than 2^31 tile entries");
+    ctx->fwd_entries = (int64_t)k;
+    if (k == 0) return DARBS_OK;
+
+    // 3. duplicate in depth order
+    DARBS_TRY(reserve(ctx, ctx->tile_keys, sizeof(unsigned) * 2 * (size_t)k));
+    DARBS_TRY(reserve(ctx, ctx->tile_vals, sizeof(unsigned) * 2 * (size_t)k));
+    unsigned* tk0 = (unsigned*)ctx->tile_keys.ptr;
+    unsigned* tk1 = tk0 + ctx->tile_keys.bytes / 8;
+    unsigned* tv0 = (unsigned*)ctx->tile_vals.ptr;
+    unsigned* tv1 = tv0 + ctx->tile_vals.bytes / 8;
+    duplicate_kernel<<<grid_for(n, 256), 256, 0, s>>>(n, order, offsets, rects, touched, ctx->tiles_x, tk0,
+                                                      tv0);
+    DARBS_TRY(check_launch(ctx, "duplicate_kernel"));
+
+    // 4. stable sort on the tile bits
+    cub::DoubleBuffer<unsigned> tkeys(tk0, tk1);
+    cub::DoubleBuffer<unsigned> tvals(tv0, tv1);
+    const int tbits = bits_for(tiles);
+    temp_bytes = 0;
+    DARBS_CUDA_TRY(ctx, cub::DeviceRadixSort::SortPairs(nullptr, temp_bytes, tkeys, tvals, (int)k, 0,
+                                                       tbits, s));
+    DARBS_TRY(reserve(ctx, ctx->cub_temp, temp_bytes));
+    temp_bytes = ctx->cub_temp.bytes;
+    DARBS_CUDA_TRY(ctx, cub::DeviceRadixSort::SortPairs(ctx->cub_temp.ptr, temp_bytes, tkeys, tvals,
+                                                       (int)k, 0, tbits, s));
+    ctx->launches += 1 + (tbits + 7) / 8;
+    ctx->cur_key_buf = tvals.Current() == tv0 ? 0 : 1;
+    const unsigned* sorted_tiles = tkeys.Current();
+
+    // 5. ranges
+    ranges_kernel<<<grid_for((int64_t)k, 256), 256, 0, s>>>((int64_t)k, sorted_tiles,
+                                                            (int2*)ctx->ranges.ptr);
+    return check_launch(ctx, "ranges_kernel");
+}
+
+darbs_status export_bins(darbs_cuda_ctx* ctx, int64_t n, int32_t* tile_ranges, int32_t* point_list,
+                         uint64_t* sort_keys, int32_t* depth_order) {
+    cudaStream_t s = ctx->stream;
+    const int tiles = ctx->tiles_x * ctx->tiles_y;
+    const int64_t k = ctx->fwd_entries;
+    if (tile_ranges && tiles)
+        DARBS_CUDA_TRY(ctx, cudaMemcpyAsync(tile_ranges, ctx->ranges.ptr, sizeof(int2) * (size_t)tiles,
+                                            cudaMemcpyDeviceToDevice, s));
+    if (depth_order && n)
+        DARBS_CUDA_TRY(ctx, cudaMemcpyAsync(depth_order, depth_order_ptr(ctx), sizeof(int32_t) * (size_t)n,
+                                            cudaMemcpyDeviceToDevice, s));
+    if (point_list && k)
+        DARBS_CUDA_TRY(ctx, cudaMemcpyAsync(point_list, point_list_ptr(ctx), sizeof(int32_t) * (size_t)k,
+                                            cudaMemcpyDeviceToDevice, s));
+    if (sort_keys && k) {
+        // rank_of[] reuses the inactive half of the order double buffer
+        unsigned* or0 = (unsigned*)ctx->order.ptr;
+        unsigned* rank_of = or0 + (size_t)(1 - ctx->cur_order_buf) * (ctx->order.bytes / 8);
+        invert_order_kernel<<<grid_for(n, 256), 256, 0, s>>>(n, depth_order_ptr(ctx), rank_of);
+        DARBS_TRY(check_launch(ctx, "invert_order_kernel"));
+        const unsigned* tk0 = (const unsigned*)ctx->tile_keys.ptr;
+        const unsigned* sorted_tiles = tk0 + (size_t)ctx->cur_key_buf * (ctx->tile_keys.bytes / 8);
+        export_keys_kernel<<<grid_for(k, 256), 256, 0, s>>>(k, sorted_tiles,
+                                                            (const unsigned*)point_list_ptr(ctx), rank_of,
+                                                            (unsigned long long*)sort_keys);
+        DARBS_TRY(check_launch(ctx, "export_keys_kernel"));
+    }
+    return DARBS_OK;
+}
+
+}  // namespace darbs_b200
