@@ -1,0 +1,462 @@
+#!/usr/bin/env python
+"""bench.py — the reference's headline workload on the B200-native rasterizer.
+
+Workload (BASELINE.json configs[2], the configuration the metric "train iters/sec (fwd+bwd) at
+1M splats 1080p per DARBF kernel" is quoted on): 1 000 000 synthetic primitives, 1920x1080, one
+camera view per GPU, one full training iteration per DARBF kernel = preprocess -> bin/sort ->
+render forward -> L1 loss -> render backward -> preprocess backward -> Adam
+(fit_scene's evaluate + adam_step, src/fit3d.cpp:104-184).  One "step" runs that iteration once
+for each of the four kernels (gaussian, half-cosine-sq, raised-cosine, inv-multiquadratic);
+``value`` = view-iterations per second over the whole job (4 * steps * n_gpus / seconds), i.e. the
+harmonic mean over the four kernels; per-kernel numbers are in ``per_kernel``.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W]            (torchrun for N > 1)
+  python bench.py --impl reference ...   times the reference's own CPU code (oracle/_ref) on the
+                                         host cores on a bounded 1/16 sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+KERNELS = ["gaussian", "half-cosine-sq", "raised-cosine", "inv-multiquadratic"]
+# algorithmic flops / MUFU ops per visit and per contributor, SURVEY.md §8d
+F_K = {"gaussian": (1, 1), "half-cosine-sq": (3, 1), "raised-cosine": (5, 2), "inv-multiquadratic": (2, 1)}
+FP_K = {"gaussian": (1, 0), "half-cosine-sq": (2, 1), "raised-cosine": (4, 2), "inv-multiquadratic": (3, 0)}
+METRIC = "train_view_iters_per_sec_1M_splats_1080p"
+UNIT = "view-iters/s (fwd+bwd+Adam, mean over the 4 DARBF kernels)"
+SAMPLE_FRACTION = 16
+
+
+def parse_args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--splats", type=int, default=1_000_000)
+    ap.add_argument("--width", type=int, default=1920)
+    ap.add_argument("--height", type=int, default=1080)
+    ap.add_argument("--focal", type=float, default=1600.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--exact", type=int, default=1, help="FP64 guard-band re-decisions (default on)")
+    return ap.parse_args()
+
+
+# ------------------------------------------------------------------------------------- clocks
+class ClockSampler:
+    """Samples nvidia-smi clocks and throttle reasons during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index, self.proc, self.lines = index, None, []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except OSError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self) -> dict:
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm, mx, pw, reasons = [], [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 7:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx.append(float(f[1]))
+                pw.append(float(f[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        # "under load": samples in the upper half of the power draw seen
+        thr = 0.5 * (min(pw) + max(pw))
+        load = [s for s, p in zip(sm, pw) if p >= thr] or sm
+        return {"sm_mhz": float(np.median(load)), "sm_max_mhz": float(max(mx)), "reasons": sorted(reasons),
+                "samples": len(sm), "power_w_max": float(max(pw))}
+
+
+# --------------------------------------------------------------------------- CPU reference arm
+def cpu_iteration(orc, cpu, name, raw64, cam, target, lrs64, state, threads):
+    """fit_scene's evaluate (one view) + adam_step, built from the oracle library's functions
+    exactly as src/fit3d.cpp:104-184 sequences them.  Returns seconds."""
+    k = orc.preset(name)
+    psi = orc.default_psi(name)
+    w, h = int(cam[4]), int(cam[5])
+    t0 = time.perf_counter()
+    prims = orc.realize(raw64)
+    st, pr = orc.project(k, psi, prims, cam)
+    vis = np.flatnonzero(pr["valid"]).astype(np.int32)
+    s = cpu.Scene(pr["mu2"][vis], None, pr["conic"][vis], pr["radius"][vis], pr["depth"][vis], prims[vis, 10],
+                  prims[vis, 11:14])
+    fr = orc.forward(k, s, w, h, (0.0, 0.0, 0.0), threads=threads, keep=True)
+    d = fr["image"] - target
+    gimg = np.sign(d) / d.size  # loss.cpp:183-188 with lambda = 0
+    st, sg = orc.backward(fr["handle"], k, gimg, s, threads=threads)
+    orc.forward_free(fr["handle"])
+    grads = orc.param_grads(psi, vis, sg, s.conic, s.opacity, s.rgb, prims, cam)
+    state["t"] += 1
+    st, p, m, v = orc.adam_step(raw64.reshape(-1), grads.reshape(-1), state["m"], state["v"], lrs64.reshape(-1),
+                                state["t"])
+    state["m"], state["v"] = m, v
+    raw64[...] = p.reshape(raw64.shape)
+    return time.perf_counter() - t0, int(fr["processed"].sum())
+
+
+def cpu_setup(args):
+    from oracle import cpu
+    from paper_2501_12369_b200 import synthetic as syn
+
+    kind = "reference" if cpu.available("reference") else "port"
+    orc = cpu.load(kind)
+    smp = syn.sample_workload(args.splats, args.width, args.height, args.focal, SAMPLE_FRACTION)
+    truth = syn.scene_b(smp["n"], 1, half_extent=smp["half_extent"])
+    cam = syn.orbit_camera(0, 1, smp["width"], smp["height"], smp["focal"])
+    init = syn.perturb(truth, 2)
+    lrs = syn.learning_rates(init)
+    return cpu, orc, kind, smp, truth, cam, init, lrs
+
+
+def cpu_target(orc, cpu, name, truth, cam, threads):
+    k = orc.preset(name)
+    psi = orc.default_psi(name)
+    prims = orc.realize(truth.astype(np.float64))
+    st, pr = orc.project(k, psi, prims, cam)
+    vis = np.flatnonzero(pr["valid"])
+    s = cpu.Scene(pr["mu2"][vis], None, pr["conic"][vis], pr["radius"][vis], pr["depth"][vis], prims[vis, 10],
+                  prims[vis, 11:14])
+    return orc.forward(k, s, int(cam[4]), int(cam[5]), (0.0, 0.0, 0.0), threads=threads)["image"]
+
+
+def run_reference_arm(args):
+    """--impl reference: the reference's own CPU implementation, all host threads."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    threads = os.cpu_count() or 1
+    cpu, orc, kind, smp, truth, cam, init, lrs = cpu_setup(args)
+    total, per_kernel = 0.0, {}
+    for name in KERNELS:
+        target = cpu_target(orc, cpu, name, truth, cam, threads)
+        raw = init.astype(np.float64).copy()
+        state = {"m": np.zeros(raw.size), "v": np.zeros(raw.size), "t": 0}
+        for _ in range(args.warmup):
+            cpu_iteration(orc, cpu, name, raw, cam, target, lrs.astype(np.float64), state, threads)
+        sec = 0.0
+        for _ in range(args.steps):
+            dt, _v = cpu_iteration(orc, cpu, name, raw, cam, target, lrs.astype(np.float64), state, threads)
+            sec += dt
+        per_kernel[name] = {"ms_per_iter_sample": 1e3 * sec / args.steps,
+                            "iters_per_s_full_equiv": args.steps / sec / SAMPLE_FRACTION}
+        total += sec
+    value = len(KERNELS) * args.steps / total / SAMPLE_FRACTION
+    sample = (f"1/{SAMPLE_FRACTION} of the workload at equal splat density: {smp['n']} primitives, "
+              f"{smp['width']}x{smp['height']}, full training iteration per kernel; value scaled by 1/{SAMPLE_FRACTION}")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps * SAMPLE_FRACTION,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": workload_config(args, args.gpus),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": kind, "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "per_kernel": per_kernel,
+    }
+    print(json.dumps(line), flush=True)
+
+
+def workload_config(args, n_gpus):
+    return {
+        "workload": f"{args.splats} synthetic 3-D primitives (scene B, SURVEY 8d), {args.width}x{args.height}, "
+                    f"1 orbit view per GPU, full training iteration (preprocess, bin+sort, render fwd, L1 loss, "
+                    f"render bwd, preprocess bwd, Adam) for each of {', '.join(KERNELS)}",
+        "splats": args.splats, "width": args.width, "height": args.height, "views_per_step": n_gpus,
+        "parallelism": f"view-parallel x{n_gpus}, NCCL all-reduce of 14N f32 parameter gradients" if n_gpus > 1
+        else "single GPU",
+        "l2_policy": "inputs larger than L2: ~0.5 GB of parameters, Adam state, records and images are "
+                     "streamed every iteration (L2 is 126 MB)",
+    }
+
+
+# -------------------------------------------------------------------------------- the GPU arm
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2501_12369_b200 as darbs
+    from paper_2501_12369_b200 import synthetic as syn
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    ctx = darbs.Context(local)
+    stream = torch.cuda.Stream(dev)  # one stream for torch ops, NCCL hand-off and the library's kernels
+    torch.cuda.set_stream(stream)
+    ctx.use_torch_stream()
+    ctx.set_exact_decisions(bool(args.exact))
+
+    n, w, h = args.splats, args.width, args.height
+    truth = syn.scene_b(n, 1)
+    init = syn.perturb(truth, 2)
+    lrs = torch.from_numpy(syn.learning_rates(init).reshape(-1)).to(dev)
+    cam = syn.orbit_camera(rank, max(world, 1), w, h, args.focal)  # view v -> rank v mod G
+    truth_d = torch.from_numpy(truth).to(dev)
+    bg = (0.0, 0.0, 0.0)  # fit_scene's background, fit3d.cpp:52
+
+    kernels = {name: (darbs.kernel_preset(name), darbs.default_psi(name)) for name in KERNELS}
+    state = {}
+    for name, (k, psi) in kernels.items():
+        target = torch.empty((h, w, 3), dtype=torch.float32, device=dev)
+        ctx.evaluate_view(k, psi, truth_d, cam, bg, grad_image=torch.zeros_like(target), image_out=target)
+        state[name] = dict(
+            params=torch.from_numpy(init).to(dev).clone(), m=torch.zeros(14 * n, device=dev),
+            v=torch.zeros(14 * n, device=dev), grads=torch.zeros((n, 14), device=dev), target=target,
+            target_host=target.cpu().pin_memory(), t=0)
+    torch.cuda.synchronize()
+
+    def iteration(name, e2e: bool):
+        k, psi = kernels[name]
+        s = state[name]
+        s["grads"].zero_()
+        if e2e:
+            # the view's target image comes from pinned host memory through the C ABI
+            # (image_space = DARBS_HOST), the loss is read back to the host
+            loss = ctx.evaluate_view(k, psi, s["params"], cam, bg, target=s["target_host"].numpy(), lam=0.0,
+                                     param_grads=s["grads"])
+        else:
+            loss = ctx.evaluate_view(k, psi, s["params"], cam, bg, target=s["target"], lam=0.0,
+                                     param_grads=s["grads"], want_loss=False)
+        if world > 1:
+            dist.all_reduce(s["grads"], op=dist.ReduceOp.SUM)  # gradients are summed over views, fit3d.cpp:148-158
+        s["t"] += 1
+        ctx.adam_step(s["params"].view(-1), s["grads"].view(-1), s["m"], s["v"], lrs, s["t"])
+        return loss
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def timed(steps, e2e):
+        """K steps (each = one iteration per kernel), CUDA events on the launching stream."""
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in KERNELS]
+        per = {name: 0.0 for name in KERNELS}
+        barrier()
+        l0 = ctx.launch_count()
+        t_start = torch.cuda.Event(enable_timing=True)
+        t_end = torch.cuda.Event(enable_timing=True)
+        t_start.record()
+        for _ in range(steps):
+            for (a, b), name in zip(ev, KERNELS):
+                a.record()
+                iteration(name, e2e)
+                b.record()
+            torch.cuda.synchronize()
+            for (a, b), name in zip(ev, KERNELS):
+                per[name] += a.elapsed_time(b)
+        t_end.record()
+        barrier()
+        ms = t_start.elapsed_time(t_end)
+        if world > 1:
+            t = torch.tensor([ms], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+        return ms, per, ctx.launch_count() - l0
+
+    # warm-up (also sizes the workspace), then the device-resident timed region.  nvidia-smi needs
+    # a few hundred ms to deliver its first sample, so the sampler runs from the warm-up on.
+    sampler = ClockSampler(local)
+    if rank == 0:
+        sampler.start()
+    for _ in range(max(args.warmup, 3)):
+        for name in KERNELS:
+            iteration(name, False)
+    ms, per, launches = timed(args.steps, e2e=False)
+    value = len(KERNELS) * args.steps * world / (ms * 1e-3)
+
+    # end-to-end: target image from pinned host memory each iteration, loss read back
+    for name in KERNELS:
+        iteration(name, True)
+    ms_e2e, per_e2e, _ = timed(args.steps, e2e=True)
+    clocks = sampler.stop() if rank == 0 else None
+    e2e_value = len(KERNELS) * args.steps * world / (ms_e2e * 1e-3)
+
+    # per-stage device times and work counters (separate, untimed pass with stage events on)
+    ctx.set_stage_timing(True)
+    peaks = ctx.microbench()
+    per_kernel = {}
+    for name in KERNELS:
+        k, psi = kernels[name]
+        s = state[name]
+        acc = None
+        reps = 3
+        for _ in range(reps):
+            s["grads"].zero_()
+            ctx.evaluate_view(k, psi, s["params"], cam, bg, target=s["target"], lam=0.0, param_grads=s["grads"])
+            st = ctx.stage_times()
+            ctx.adam_step(s["params"].view(-1), s["grads"].view(-1), s["m"], s["v"], lrs, s["t"] + 1)
+            st["adam"] = ctx.stage_times()["adam"]
+            acc = st if acc is None else {kk: acc[kk] + st[kk] for kk in st}
+        st = {kk: vv / reps for kk, vv in acc.items()}
+        wc = ctx.work_counters()
+        V, Cn = wc["visits"], wc["contributors"]
+        fk, sk = F_K[name]
+        fpk, spk = FP_K[name]
+        flops_fwd = V * (13 + fk) + 9 * Cn
+        flops_bwd = V * (13 + fk + fpk) + 57 * Cn
+        mufu_fwd, mufu_bwd = V * sk, V * (sk + spk) + Cn
+        fp32_peak = 2.0 * peaks["ffma_per_s"]
+
+        def roof(flops, mufu, ms_k):
+            t_fp = flops / fp32_peak
+            t_mu = mufu / peaks["mufu_per_s"]
+            return {"ms": ms_k, "algorithmic_gflop": flops / 1e9, "achieved_tflops": flops / (ms_k * 1e-3) / 1e12,
+                    "frac_fp32": t_fp / (ms_k * 1e-3), "frac_mufu": t_mu / (ms_k * 1e-3),
+                    "frac": max(t_fp, t_mu) / (ms_k * 1e-3)}
+
+        per_kernel[name] = {
+            "iters_per_s": args.steps * world / (per[name] * 1e-3),
+            "iters_per_s_e2e": args.steps * world / (per_e2e[name] * 1e-3),
+            "ms_per_iter": per[name] / args.steps,
+            "stage_ms": st,
+            "render_fps": 1e3 / max(st["preprocess"] + st["binning"] + st["render_fwd"], 1e-9),
+            "work": wc,
+            "render_fwd": roof(flops_fwd, mufu_fwd, st["render_fwd"]),
+            "render_bwd": roof(flops_bwd, mufu_bwd, st["render_bwd"]),
+        }
+    ctx.set_stage_timing(False)
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+
+    # dominant kernel = the render kernel with the largest device time over the four families
+    dom = max(((nm, kk) for nm in KERNELS for kk in ("render_fwd", "render_bwd")),
+              key=lambda t: per_kernel[t[0]][t[1]]["ms"])
+    dk = per_kernel[dom[0]][dom[1]]
+    roofline = {
+        "bound": "fp32", "kernel": f"{dom[1]}<{dom[0]}>", "achieved": dk["achieved_tflops"],
+        "peak": 2.0 * peaks["ffma_per_s"] / 1e12, "unit": "TFLOP/s", "frac": dk["frac"], "traffic": None,
+        "frac_fp32": dk["frac_fp32"], "frac_mufu": dk["frac_mufu"],
+        "peak_source": "measured live by darbs_cuda_microbench (register-operand FFMA x2; MUFU ex2.approx); "
+                       "MEASURED_PEAKS.json has no FP32/MUFU entry",
+        "peak_mufu_gops": peaks["mufu_per_s"] / 1e9, "peak_sm_mhz": peaks["sm_mhz"],
+        "peak_ffma_imm_tflops": 2.0 * peaks["ffma_imm_per_s"] / 1e12,
+        "algorithmic_work": "flops = V*(13+F_k[+F'_k]) + {9|57}*C per launch with V = sum processed, C = sum "
+                            "contributors of that launch (SURVEY 8d); frac = max(flops/peak_fp32, mufu/peak_mufu)/t",
+    }
+
+    hbm_peak = None
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            hbm_peak = json.load(f).get("hbm_gbs")
+    except OSError:
+        pass
+    if hbm_peak:
+        # streaming stages against the measured HBM peak (algorithmic bytes)
+        for name in KERNELS:
+            st = per_kernel[name]["stage_ms"]
+            kk = per_kernel[name]["work"]["entries"]
+            per_kernel[name]["hbm_frac"] = {
+                "preprocess": (56 + 48) * n / (st["preprocess"] * 1e-3) / 1e9 / hbm_peak,
+                "preprocess_bwd": (36 + 56 + 56) * n / (st["preprocess_bwd"] * 1e-3) / 1e9 / hbm_peak,
+                "adam": 28 * 14 * n / (st["adam"] * 1e-3) / 1e9 / hbm_peak,
+                # rect 60 B + depth sort (4 digit passes x 16 B + 4 B histogram read) + pack 108 B per
+                # splat; duplicate 8 B + tile sort (2 passes x 16 B + 4 B) + ranges 4 B per tile entry
+                "binning_sort": (236 * n + 48 * kk) / (st["binning"] * 1e-3) / 1e9 / hbm_peak,
+            }
+
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": max(args.warmup, 3), "ms_per_step": ms / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": workload_config(args, world), "clocks": clocks,
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": len(KERNELS) * 12 * w * h,
+                "d2h_bytes_per_step": len(KERNELS) * 32,
+                "path": "darbs_cuda_evaluate_view with the view's target image in pinned host memory "
+                        "(image_space = DARBS_HOST) and the loss read back; parameters stay on the device"},
+        "gpu_launches": int(launches),
+        "roofline": roofline,
+        "exact_decisions": bool(args.exact),
+        "per_kernel": per_kernel,
+    }
+    if world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(args)
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def cpu_baseline(args):
+    """The reference's CPU code on this box's host cores, bounded to ~10-30 s: one training
+    iteration per kernel on the 1/16 sample (plus one warm-up for the first kernel)."""
+    threads = os.cpu_count() or 1
+    cpu, orc, kind, smp, truth, cam, init, lrs = cpu_setup(args)
+    total, iters = 0.0, 0
+    t_budget = time.perf_counter()
+    for name in KERNELS:
+        target = cpu_target(orc, cpu, name, truth, cam, threads)
+        raw = init.astype(np.float64).copy()
+        state = {"m": np.zeros(raw.size), "v": np.zeros(raw.size), "t": 0}
+        reps = 2 if time.perf_counter() - t_budget < 20 else 1
+        for _ in range(reps):
+            dt, _v = cpu_iteration(orc, cpu, name, raw, cam, target, lrs.astype(np.float64), state, threads)
+            total += dt
+            iters += 1
+    value = iters / total / SAMPLE_FRACTION
+    return {"value": value, "unit": UNIT, "cores": threads, "kind": kind,
+            "sample": f"1/{SAMPLE_FRACTION} of the workload at equal splat density ({smp['n']} primitives, "
+                      f"{smp['width']}x{smp['height']}), {iters} full training iterations over the 4 kernels, "
+                      f"value scaled by 1/{SAMPLE_FRACTION}"}
+
+
+def main():
+    args = parse_args()
+    if args.impl == "reference":
+        run_reference_arm(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -100,7 +100,8 @@ DARBS_API void darbs_cuda_destroy(darbs_cuda_ctx* ctx);
  * NULL for create failures. */
 DARBS_API const char* darbs_cuda_last_error(const darbs_cuda_ctx* ctx);
 /* Use an externally owned cudaStream_t (e.g. torch's current stream) for all
- * subsequent work; NULL restores the context's own stream. */
+ * subsequent work; NULL restores the context's own stream.  To run on the legacy
+ * default stream pass cudaStreamLegacy ((void*)1), not NULL. */
 DARBS_API darbs_status darbs_cuda_set_stream(darbs_cuda_ctx* ctx, void* cuda_stream);
 DARBS_API darbs_status darbs_cuda_synchronize(darbs_cuda_ctx* ctx);
 /* Number of kernels this library has launched on the context since creation
@@ -201,7 +202,9 @@ DARBS_API darbs_status darbs_cuda_backward_projection(darbs_cuda_ctx* ctx, doubl
  *   realize -> project_primitive (near-plane cull) -> forward -> loss ->
  *   backward -> conic-grad -> cov2-grad -> backward_projection ->
  *   reparametrisation -> param_grads[14n] += .
- * raw_params[14n] and param_grads[14n] follow `space`.  Exactly one of
+ * raw_params[14n] and param_grads[14n] follow `param_space`; target, grad_image
+ * and image_out follow `image_space` (a training loop keeps the parameters on the
+ * device and feeds each view's target image from the host).  Exactly one of
  * `target` / `grad_image` is non-NULL:
  *   target     [3wh]: loss_total(image, target, lambda) (src/loss.cpp:173-230)
  *                     drives the backward; *loss_out receives total, l1, dssim, mse.
@@ -218,7 +221,8 @@ DARBS_API darbs_status darbs_cuda_evaluate_view(darbs_cuda_ctx* ctx,
                                                 const float* target, double lambda,
                                                 const float* grad_image, float* param_grads,
                                                 float* image_out, double loss_out[4],
-                                                darbs_space space);
+                                                darbs_space param_space,
+                                                darbs_space image_space);
 
 /* adam_step, include/darbs/optim.hpp:24-39 (beta1 .9, beta2 .999, eps 1e-15,
  * per-parameter learning rates, t is 1-based). */
@@ -240,6 +244,14 @@ DARBS_API darbs_status darbs_cuda_stage_times(darbs_cuda_ctx* ctx, double out_ms
  * re-decisions, out[5] = pixels flagged near the transmittance floor.
  * Synchronises. */
 DARBS_API darbs_status darbs_cuda_work_counters(darbs_cuda_ctx* ctx, int64_t out[8]);
+
+/* Register-only micro-benchmarks of the two pipes that bound the render kernels,
+ * run on the context's GPU (a few milliseconds): out[0] = FP32 FMA instructions
+ * per second with register operands (x2 = FLOP/s), out[1] = MUFU (ex2.approx)
+ * operations per second, out[2] = SM clock in MHz seen by the FMA loop (clock64
+ * span / event time), out[3] = number of SMs, out[4] = FP32 FMA instructions per
+ * second in the immediate-operand form. */
+DARBS_API darbs_status darbs_cuda_microbench(darbs_cuda_ctx* ctx, double out[8]);
 
 #ifdef __cplusplus
 }

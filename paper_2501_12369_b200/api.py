@@ -95,7 +95,8 @@ def _load():
     lib.darbs_cuda_project.argtypes = [vp, ks, dbl, dbl, i64, vp, C.POINTER(dbl), vp, vp, vp, vp, vp, vp, i32]
     lib.darbs_cuda_backward_projection.argtypes = [vp, dbl, i64, vp, vp, vp, C.POINTER(dbl), vp, vp, vp, i32]
     lib.darbs_cuda_evaluate_view.argtypes = [vp, ks, dbl, i64, vp, C.POINTER(dbl), C.POINTER(C.c_float), vp,
-                                             dbl, vp, vp, vp, C.POINTER(dbl), i32]
+                                             dbl, vp, vp, vp, C.POINTER(dbl), i32, i32]
+    lib.darbs_cuda_microbench.argtypes = [vp, C.POINTER(dbl)]
     lib.darbs_cuda_adam_step.argtypes = [vp, i64, vp, vp, vp, vp, vp, i32, i32]
     lib.darbs_cuda_set_stage_timing.argtypes = [vp, i32]
     lib.darbs_cuda_stage_times.argtypes = [vp, C.POINTER(dbl)]
@@ -111,7 +112,7 @@ EXPORTED_SYMBOLS = (
     "darbs_cuda_kernel_preset darbs_cuda_default_psi darbs_cuda_eval darbs_cuda_bin darbs_cuda_forward "
     "darbs_cuda_backward darbs_cuda_realize darbs_cuda_project darbs_cuda_backward_projection "
     "darbs_cuda_evaluate_view darbs_cuda_adam_step darbs_cuda_set_stage_timing darbs_cuda_stage_times "
-    "darbs_cuda_work_counters"
+    "darbs_cuda_work_counters darbs_cuda_microbench"
 ).split()
 
 
@@ -253,9 +254,12 @@ class Context:
         self._check(_lib.darbs_cuda_set_stream(self._h, C.c_void_p(cuda_stream or 0)))
 
     def use_torch_stream(self):
+        """Run on torch's current stream.  torch's default stream is the legacy NULL stream,
+        which the ABI spells cudaStreamLegacy (1) because NULL means "the context's own"."""
         import torch
 
-        self.set_stream(torch.cuda.current_stream(self.device).cuda_stream)
+        h = torch.cuda.current_stream(self.device).cuda_stream
+        self.set_stream(h if h else 1)
 
     def synchronize(self):
         self._check(_lib.darbs_cuda_synchronize(self._h))
@@ -274,6 +278,12 @@ class Context:
         self._check(_lib.darbs_cuda_stage_times(self._h, out))
         names = ["preprocess", "binning", "render_fwd", "loss", "render_bwd", "preprocess_bwd", "adam"]
         return {k: float(out[i]) for i, k in enumerate(names)}
+
+    def microbench(self) -> dict:
+        out = (C.c_double * 8)()
+        self._check(_lib.darbs_cuda_microbench(self._h, out))
+        return dict(ffma_per_s=float(out[0]), mufu_per_s=float(out[1]), sm_mhz=float(out[2]), sms=int(out[3]),
+                    ffma_imm_per_s=float(out[4]))
 
     def work_counters(self) -> dict:
         out = (C.c_int64 * 8)()
@@ -406,19 +416,20 @@ class Context:
                       target=None, lam: float = 0.0, grad_image=None, param_grads=None, image_out=None,
                       want_loss: bool = True):
         """One view of fit_scene's evaluate, src/fit3d.cpp:108-159.  Returns (total, l1, dssim, mse)."""
-        a = _Args()
+        a, ai = _Args(), _Args()  # parameters and images may live in different spaces
         n = (raw_params.numel() if _is_torch(raw_params) else np.asarray(raw_params).size) // 14
         cam, pcam = _cam(camera)
         w, h = int(cam[4]), int(cam[5])
         p_raw = a.ptr(raw_params, np.float32, 14 * n)
-        p_t = a.ptr(target, np.float32, 3 * w * h)
-        p_g = a.ptr(grad_image, np.float32, 3 * w * h)
+        p_t = ai.ptr(target, np.float32, 3 * w * h)
+        p_g = ai.ptr(grad_image, np.float32, 3 * w * h)
         p_pg = a.inout(param_grads, np.float32, 14 * n)
-        p_img = a.inout(image_out, np.float32, 3 * w * h)
+        p_img = ai.inout(image_out, np.float32, 3 * w * h)
         bg = (C.c_float * 3)(*[float(x) for x in background])
         loss = (C.c_double * 4)()
         self._check(_lib.darbs_cuda_evaluate_view(self._h, C.byref(kernel), psi, n, p_raw, pcam, bg, p_t, lam,
-                                                  p_g, p_pg, p_img, loss if want_loss else None, a.space))
+                                                  p_g, p_pg, p_img, loss if want_loss else None, a.space,
+                                                  ai.space if ai.space is not None else a.space))
         return tuple(float(x) for x in loss)
 
     def adam_step(self, params, grads, m, v, lrs, t: int):

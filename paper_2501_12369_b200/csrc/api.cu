@@ -638,7 +638,8 @@ darbs_status darbs_cuda_evaluate_view(darbs_cuda_ctx* ctx, const darbs_kernel_sp
                                       int64_t n, const float* raw_params, const double* camera,
                                       const float background[3], const float* target, double lambda,
                                       const float* grad_image, float* param_grads, float* image_out,
-                                      double loss_out[4], darbs_space space) {
+                                      double loss_out[4], darbs_space param_space,
+                                      darbs_space image_space) {
     CTX_OR_FAIL(ctx);
     if (!camera || !background) return fail(ctx, DARBS_INVALID_PARAMETER, "camera/background is NULL");
     if ((target != nullptr) == (grad_image != nullptr))
@@ -656,14 +657,17 @@ darbs_status darbs_cuda_evaluate_view(darbs_cuda_ctx* ctx, const darbs_kernel_sp
     const size_t px = (size_t)width * height, nn = (size_t)n;
     reset_stage_marks(ctx, {ST_PREPROCESS, ST_BINNING, ST_RENDER_FWD, ST_LOSS, ST_RENDER_BWD, ST_PREPROCESS_BWD});
 
-    Stager st(ctx, space);
+    Stager st(ctx, param_space);
+    Stager sti(ctx, image_space);
+    sti.in_slot = 4;   // the two stagers share the context's staging slots
+    sti.out_slot = 4;
     const float *d_raw, *d_target, *d_gimg;
     float *d_pgrads, *d_image;
     DARBS_TRY(st.in(raw_params, 14 * nn, &d_raw));
-    DARBS_TRY(st.in(target, 3 * px, &d_target));
-    DARBS_TRY(st.in(grad_image, 3 * px, &d_gimg));
+    DARBS_TRY(sti.in(target, 3 * px, &d_target));
+    DARBS_TRY(sti.in(grad_image, 3 * px, &d_gimg));
     DARBS_TRY(st.inout(param_grads, 14 * nn, &d_pgrads));
-    DARBS_TRY(st.out(image_out, 3 * px, &d_image));
+    DARBS_TRY(sti.out(image_out, 3 * px, &d_image));
 
     // internal SoA of the projected splats (one slot each; no compaction)
     DARBS_TRY(reserve(ctx, ctx->valid, sizeof(int32_t) * nn + sizeof(float) * 11 * nn));
@@ -711,6 +715,7 @@ darbs_status darbs_cuda_evaluate_view(darbs_cuda_ctx* ctx, const darbs_kernel_sp
         }
     }
     DARBS_TRY(st.finish());
+    DARBS_TRY(sti.finish());
     if (loss_out) {
         // flags (2 ints) and loss sums (2 doubles) in one pinned read
         DARBS_CUDA_TRY(ctx, cudaMemcpyAsync(ctx->pinned, d_flags, 32, cudaMemcpyDeviceToHost, ctx->stream));

@@ -1,0 +1,112 @@
+// microbench.cu — register-only micro-benchmarks of the FP32 FMA pipe and the
+// MUFU (special-function) pipe.  The render kernels are bound by the issue rate
+// of these two pipes, not by HBM or tensor cores, and MEASURED_PEAKS.json has no
+// entry for them (SURVEY.md §8d asks the build to measure them on the box).
+#include "common.cuh"
+
+namespace darbs_b200 {
+namespace {
+
+constexpr int kIters = 4096;
+
+// 8 independent FMA chains per thread: no dependency stalls at 4-cycle latency
+// with >= 8 warps per scheduler.
+// IMM = true lets ptxas use the immediate-operand FFMA form; IMM = false keeps
+// both multiplier and addend in registers (the form the render kernels issue).
+template <bool IMM>
+__global__ void __launch_bounds__(1024) ffma_kernel(float seed, float* sink, long long* cycles) {
+    float a0 = seed + threadIdx.x, a1 = a0 + 1.f, a2 = a0 + 2.f, a3 = a0 + 3.f;
+    float a4 = a0 + 4.f, a5 = a0 + 5.f, a6 = a0 + 6.f, a7 = a0 + 7.f;
+    const float m = IMM ? 0.999f : 0.999f + (float)(blockIdx.x >> 30);
+    const float c = IMM ? 0.001f : 0.001f + (float)(blockIdx.x >> 29);
+    long long t0 = clock64();
+#pragma unroll 1
+    for (int i = 0; i < kIters; ++i) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            a0 = fmaf(a0, m, c);
+            a1 = fmaf(a1, m, c);
+            a2 = fmaf(a2, m, c);
+            a3 = fmaf(a3, m, c);
+            a4 = fmaf(a4, m, c);
+            a5 = fmaf(a5, m, c);
+            a6 = fmaf(a6, m, c);
+            a7 = fmaf(a7, m, c);
+        }
+    }
+    long long t1 = clock64();
+    float s = a0 + a1 + a2 + a3 + a4 + a5 + a6 + a7;
+    if (s == 12345.678f) sink[0] = s;  // keep the chains alive
+    if (blockIdx.x == 0 && threadIdx.x == 0) cycles[0] = t1 - t0;
+}
+
+__global__ void __launch_bounds__(1024) mufu_kernel(float seed, float* sink) {
+    float a0 = seed + 1e-3f * threadIdx.x, a1 = a0 - 0.1f, a2 = a0 - 0.2f, a3 = a0 - 0.3f;
+#pragma unroll 1
+    for (int i = 0; i < kIters; ++i) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            asm volatile("ex2.approx.ftz.f32 %0, %0;" : "+f"(a0));
+            asm volatile("ex2.approx.ftz.f32 %0, %0;" : "+f"(a1));
+            asm volatile("ex2.approx.ftz.f32 %0, %0;" : "+f"(a2));
+            asm volatile("ex2.approx.ftz.f32 %0, %0;" : "+f"(a3));
+        }
+    }
+    float s = a0 + a1 + a2 + a3;
+    if (s == 12345.678f) sink[0] = s;
+}
+
+}  // namespace
+}  // namespace darbs_b200
+
+using namespace darbs_b200;
+
+extern "C" darbs_status darbs_cuda_microbench(darbs_cuda_ctx* ctx, double out[8]) {
+    if (!ctx) return fail(nullptr, DARBS_INVALID_PARAMETER, "context is NULL");
+    int prev = -1;
+    cudaGetDevice(&prev);
+    if (prev != ctx->device) cudaSetDevice(ctx->device);
+    cudaDeviceProp prop;
+    DARBS_CUDA_TRY(ctx, cudaGetDeviceProperties(&prop, ctx->device));
+    const int sms = prop.multiProcessorCount;
+    const int blocks = sms * 2, threads = 1024;  // 2 x 1024 threads = full occupancy
+    float* sink = (float*)((unsigned long long*)ctx->counters.ptr + 20);
+    long long* cycles = (long long*)((unsigned long long*)ctx->counters.ptr + 22);
+    cudaEvent_t e0 = ctx->timer.ev[14], e1 = ctx->timer.ev[15];
+    float ms_f = 0.f, ms_m = 0.f, ms_i = 0.f;
+    for (int rep = 0; rep < 3; ++rep) {
+        DARBS_CUDA_TRY(ctx, cudaEventRecord(e0, ctx->stream));
+        ffma_kernel<true><<<blocks, threads, 0, ctx->stream>>>(1.0f, sink, cycles);
+        DARBS_CUDA_TRY(ctx, cudaEventRecord(e1, ctx->stream));
+        DARBS_CUDA_TRY(ctx, cudaEventSynchronize(e1));
+        DARBS_CUDA_TRY(ctx, cudaEventElapsedTime(&ms_i, e0, e1));
+    }
+    for (int rep = 0; rep < 3; ++rep) {  // last repetition counts (clocks ramped up)
+        DARBS_CUDA_TRY(ctx, cudaEventRecord(e0, ctx->stream));
+        ffma_kernel<false><<<blocks, threads, 0, ctx->stream>>>(1.0f, sink, cycles);
+        DARBS_CUDA_TRY(ctx, cudaEventRecord(e1, ctx->stream));
+        DARBS_CUDA_TRY(ctx, cudaEventSynchronize(e1));
+        DARBS_CUDA_TRY(ctx, cudaEventElapsedTime(&ms_f, e0, e1));
+    }
+    for (int rep = 0; rep < 3; ++rep) {
+        DARBS_CUDA_TRY(ctx, cudaEventRecord(e0, ctx->stream));
+        mufu_kernel<<<blocks, threads, 0, ctx->stream>>>(0.5f, sink);
+        DARBS_CUDA_TRY(ctx, cudaEventRecord(e1, ctx->stream));
+        DARBS_CUDA_TRY(ctx, cudaEventSynchronize(e1));
+        DARBS_CUDA_TRY(ctx, cudaEventElapsedTime(&ms_m, e0, e1));
+    }
+    DARBS_TRY(check_launch(ctx, "microbench", 9));
+    long long cyc = 0;
+    DARBS_CUDA_TRY(ctx, cudaMemcpy(&cyc, cycles, sizeof(cyc), cudaMemcpyDeviceToHost));
+    const double n_thr = (double)blocks * threads;
+    out[0] = n_thr * kIters * 32.0 / (ms_f * 1e-3);
+    out[1] = n_thr * kIters * 16.0 / (ms_m * 1e-3);
+    // one block's clock64 span of the FFMA loop over the kernel's wall time: the
+    // block runs for (almost) the whole kernel, so cycles / time ~ SM clock.
+    out[2] = (double)cyc / (ms_f * 1e-3) / 1e6;
+    out[3] = (double)sms;
+    out[4] = n_thr * kIters * 32.0 / (ms_i * 1e-3);
+    out[5] = out[6] = out[7] = 0.0;
+    if (prev >= 0 && prev != ctx->device) cudaSetDevice(prev);
+    return DARBS_OK;
+}
