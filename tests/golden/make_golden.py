@@ -1,0 +1,146 @@
+#!/usr/bin/env python
+"""Generates tests/golden/*.npz by running the REFERENCE'S OWN SOURCES.
+
+The reference (arxiv/paper_2501_12369, proj/core) ships no golden images: every known answer in
+its tests is closed-form or "reference vs its own brute-force oracle".  These
+fixtures are therefore outputs of the reference itself: oracle/_ref/libdarbs_ref.so is
+/root/reference/proj/core/src/{kernel,geometry,rasterizer}.cpp compiled unmodified against
+oracle/eigen_shim (oracle/Makefile `ref`).  /root/reference does not exist on the GPU box, so the
+vectors are committed; this script is how they were made:
+
+    make -C oracle ref && python tests/golden/make_golden.py
+
+Every input is float32-representable (SURVEY.md §8c "parity input rule"), so the same numbers feed
+the FP64 reference and the float32 C ABI.  Outputs are the reference's FP64 results.
+"""
+import os
+import sys
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(os.path.dirname(HERE))
+sys.path.insert(0, ROOT)
+
+from oracle import cpu  # noqa: E402
+
+PRESETS = ["gaussian", "half-cosine-sq", "raised-cosine", "mod-sinc", "inv-multiquadratic"]
+BG = (0.1, 0.2, 0.3)
+# proj/data/demo_cameras.txt, first block (fx fy cx cy w h + 16 row-major world-to-camera)
+DEMO_CAMERA = np.array([80, 80, 32, 32, 64, 64,
+                        -0.3894183423, 0, 0.921060994, 4.278389336e-17,
+                        -0.2646649291, 0.9578262852, -0.1118985373, -1.14366835e-16,
+                        -0.8822164303, -0.2873478856, -0.3729951242, 3.132091953,
+                        0, 0, 0, 1.0])
+
+
+def f32r(a):
+    return np.asarray(a, dtype=np.float32).astype(np.float64)
+
+
+def raster_case(ref, name, n, w, h, seed):
+    k = ref.preset(name)
+    s = ref.random_scene(k, n, w, h, seed)
+    g = ref.random_image_grad(w, h, 1000 + seed)
+    offsets, plist, order = ref.bin(s, w, h)
+    fr = ref.forward(k, s, w, h, BG, threads=1, keep=True)
+    st, grads = ref.backward(fr["handle"], k, g, s, threads=1)
+    ref.forward_free(fr["handle"])
+    assert st == 0
+    brute = ref.oracle_forward(k, s, w, h, BG)
+    return dict(
+        kernel=name, n=n, width=w, height=h, seed=seed, background=np.array(BG),
+        mu2=s.mu2.astype(np.float32), cov2=s.cov2.astype(np.float32), conic=s.conic.astype(np.float32),
+        radius=s.radius.astype(np.float32), depth=s.depth.astype(np.float32),
+        opacity=s.opacity.astype(np.float32), rgb=s.rgb.astype(np.float32), grad_image=g.astype(np.float32),
+        tile_offsets=offsets, point_list=plist, depth_order=order,
+        image=fr["image"], t_final=fr["t_final"], processed=fr["processed"], contributors=fr["contributors"],
+        skipped=fr["skipped"], brute_image=brute, splat_grads=grads)
+
+
+def geometry_case(ref, name, n, seed):
+    k = ref.preset(name)
+    psi = ref.default_psi(name)
+    rng = np.random.default_rng(seed)
+    raw = np.zeros((n, 14))
+    raw[:, 0:3] = rng.uniform(-0.9, 0.9, (n, 3))
+    raw[:, 3:6] = np.log(rng.uniform(0.02, 0.08, (n, 3)))
+    raw[:, 6:10] = rng.normal(size=(n, 4))
+    raw[:, 10] = rng.normal(size=n)
+    raw[:, 11:14] = rng.normal(size=(n, 3))
+    raw[3, 0:3] = (3.5288, 1.1492, 1.4920)  # behind the demo camera: near-plane culled
+    raw = f32r(raw)
+    prims = f32r(ref.realize(raw))  # the float32 primitives the C ABI's project() consumes
+    st, pr = ref.project(k, psi, prims, DEMO_CAMERA)
+    assert st == 0
+    gc = f32r(rng.normal(size=(n, 4)))
+    gm = f32r(rng.normal(size=(n, 2)))
+    d_mu, d_scale, d_rot = ref.backward_projection(psi, gc, gm, prims, DEMO_CAMERA)
+    # the evaluate chain (fit3d.cpp:108-159) on the reference, fed float32-rounded splats
+    prims_full = ref.realize(raw)
+    st, pf = ref.project(k, psi, prims_full, DEMO_CAMERA)
+    vis = np.flatnonzero(pf["valid"]).astype(np.int32)
+    s = cpu.Scene(f32r(pf["mu2"][vis]), None, f32r(pf["conic"][vis]), pf["radius"][vis], f32r(pf["depth"][vis]),
+                  f32r(prims_full[vis, 10]), f32r(prims_full[vis, 11:14]))
+    w, h = 64, 64
+    gimg = ref.random_image_grad(w, h, 77)
+    fr = ref.forward(k, s, w, h, (0, 0, 0), threads=1, keep=True)
+    st, sg = ref.backward(fr["handle"], k, gimg, s, threads=1)
+    ref.forward_free(fr["handle"])
+    pg = ref.param_grads(psi, vis, sg, s.conic, s.opacity, s.rgb, prims_full, DEMO_CAMERA)
+    return dict(kernel=name, psi=psi, camera=DEMO_CAMERA, raw=raw.astype(np.float32),
+                prims=prims.astype(np.float32), valid=pr["valid"], mu2=pr["mu2"], cov2=pr["cov2"],
+                conic=pr["conic"], radius=pr["radius"], depth=pr["depth"],
+                grad_cov2=gc.astype(np.float32), grad_mu2=gm.astype(np.float32), d_mu=d_mu, d_scale=d_scale,
+                d_rot=d_rot, view_grad_image=gimg.astype(np.float32), view_image=fr["image"],
+                view_param_grads=pg, view_processed=fr["processed"], view_contributors=fr["contributors"])
+
+
+def eval_case(ref):
+    out = {}
+    for name in PRESETS:
+        k = ref.preset(name)
+        dm2 = f32r(np.concatenate([np.linspace(0.0, k.cutoff * 1.5, 257), [k.cutoff, 1e-20, 0.3, 1.0, 2.5, 8.9]]))
+        st, w, dw = ref.eval(k, dm2)
+        assert st == 0
+        out[name + "/dm2"] = dm2.astype(np.float32)
+        out[name + "/weight"] = w
+        out[name + "/dweight"] = dw
+        out[name + "/spec"] = np.array([k.family, k.beta, k.xi, k.lobes, k.cutoff, k.unbounded], dtype=np.float64)
+        out[name + "/psi"] = np.array(ref.default_psi(name))
+    return out
+
+
+def adam_case(ref):
+    rng = np.random.default_rng(3)
+    dim = 14 * 64
+    p = f32r(rng.normal(size=dim))
+    g = f32r(rng.normal(size=dim))
+    lrs = f32r(rng.uniform(1e-4, 1e-2, size=dim))
+    m, v = np.zeros(dim), np.zeros(dim)
+    out = dict(params0=p.astype(np.float32), grads=g.astype(np.float32), lrs=lrs.astype(np.float32))
+    for t in (1, 2, 3):
+        st, p, m, v = ref.adam_step(p, g, m, v, lrs, t)
+        assert st == 0
+        out[f"params{t}"], out[f"m{t}"], out[f"v{t}"] = p, m, v
+    return out
+
+
+def main():
+    if not cpu.available("reference"):
+        raise SystemExit("oracle/_ref/libdarbs_ref.so missing: run `make -C oracle ref` where /root/reference exists")
+    ref = cpu.load("reference")
+    assert ref.kind == "reference"
+    for name in PRESETS:
+        for seed, (n, w, h) in enumerate([(300, 48, 40), (150, 33, 17)]):
+            np.savez_compressed(os.path.join(HERE, f"raster_{name}_{seed}.npz"), **raster_case(ref, name, n, w, h, seed))
+    for name in ["gaussian", "half-cosine-sq", "raised-cosine", "inv-multiquadratic"]:
+        np.savez_compressed(os.path.join(HERE, f"geometry_{name}.npz"), **geometry_case(ref, name, 120, 9))
+    np.savez_compressed(os.path.join(HERE, "eval.npz"), **eval_case(ref))
+    np.savez_compressed(os.path.join(HERE, "adam.npz"), **adam_case(ref))
+    total = sum(os.path.getsize(os.path.join(HERE, f)) for f in os.listdir(HERE) if f.endswith(".npz"))
+    print(f"wrote golden fixtures, {total / 1024:.0f} KiB")
+
+
+if __name__ == "__main__":
+    main()
