@@ -315,7 +315,7 @@ void darbs_cuda_destroy(darbs_cuda_ctx* ctx) {
     DeviceGuard guard(ctx->device);
     cudaStreamSynchronize(ctx->stream);
     DeviceBuffer* bufs[] = {&ctx->recs, &ctx->rects, &ctx->depth_keys, &ctx->order, &ctx->offsets,
-                            &ctx->tile_keys, &ctx->tile_vals, &ctx->ranges, &ctx->cub_temp,
+                            &ctx->tile_keys, &ctx->tile_vals, &ctx->ranges, &ctx->surv, &ctx->surv_count, &ctx->cub_temp,
                             &ctx->counters, &ctx->t_final, &ctx->processed, &ctx->contributors,
                             &ctx->image, &ctx->valid, &ctx->splat_grads, &ctx->grad_image};
     for (DeviceBuffer* b : bufs)

@@ -40,8 +40,8 @@ struct KParams {
 // Packed per-splat record, 4 x float4 = 64 B, 64-B aligned (two 32-B sectors
 // per gather for the three hot vectors):
 //   v0 = { mu.x, mu.y, A = scale*a, B = scale*2b }
-//   v1 = { C = scale*c, opacity, thr_m, 0 }     thr_m: see family_threshold()
-//   v2 = { r, g, b, 0 }
+//   v1 = { C = scale*c, opacity, thr_m, -b/c }  thr_m: see family_threshold()
+//   v2 = { r, g, b, -b/a }                       v1.w, v2.w: block-cull helpers
 //   v3 = { a, b, c, 0 }                          unscaled conic for the FP64 path
 static constexpr int kRecVecs = 4;
 
@@ -81,6 +81,8 @@ struct darbs_cuda_ctx {
     darbs_b200::DeviceBuffer tile_keys;    // 2 * K u32
     darbs_b200::DeviceBuffer tile_vals;    // 2 * K u32
     darbs_b200::DeviceBuffer ranges;       // tiles * int2
+    darbs_b200::DeviceBuffer surv;         // 8 * K int2 (splat index, list position) per-block survivor lists
+    darbs_b200::DeviceBuffer surv_count;   // 8 * tiles int
     darbs_b200::DeviceBuffer cub_temp;
     darbs_b200::DeviceBuffer counters;     // Counters + scalars
     darbs_b200::DeviceBuffer t_final, processed, contributors, image;  // per-pixel aux

@@ -30,6 +30,11 @@ __device__ __forceinline__ float rsqrt_approx(float x) {
     asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
     return y;
 }
+__device__ __forceinline__ float rcp_approx(float x) {
+    float y;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
 __device__ __forceinline__ float sqrt_approx(float x) {
     float y;
     asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -63,7 +68,7 @@ __device__ __forceinline__ void fam_eval(float m, float& w, float& dwdm) {
         w = __cosf(m);
         dwdm = -__sinf(m);
     } else if constexpr (FAM == FAM_RCOS1) {
-        float u = sqrt_approx(m);
+        float u = sqrt_approx(fmaxf(m, 0.f));  // FP32 rounding can leave m a hair below zero
         w = fmaf(0.5f, __cosf(u), 0.5f);
         // d/dm [.5 + .5 cos(sqrt m)] = -.25 sin(u)/u  -> -.25 as u -> 0 (kernel.cpp:115-116)
         dwdm = (m < 1e-12f) ? -0.25f : -0.25f * __sinf(u) * rsqrt_approx(m);
@@ -84,7 +89,7 @@ __device__ __forceinline__ float fam_weight(float m) {
     } else if constexpr (FAM == FAM_HCOS2) {
         return __cosf(m);
     } else if constexpr (FAM == FAM_RCOS1) {
-        return fmaf(0.5f, __cosf(sqrt_approx(m)), 0.5f);
+        return fmaf(0.5f, __cosf(sqrt_approx(fmaxf(m, 0.f))), 0.5f);
     } else if constexpr (FAM == FAM_IMQ) {
         return rsqrt_approx(m + 1.0f);
     } else {

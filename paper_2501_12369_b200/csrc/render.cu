@@ -53,44 +53,39 @@ __global__ void pack_kernel(KParams kp, int64_t n, const float* __restrict__ mu2
     float thr_m = pd ? (float)(thr * (double)kp.scale) : __int_as_float(0x7fc00000);
     float4* r = recs + kRecVecs * i;
     r[0] = make_float4(mx, my, kp.scale * a, kp.scale * (2.0f * b));
-    r[1] = make_float4(kp.scale * c, o, thr_m, 0.f);
-    r[2] = make_float4(rgb[3 * i], rgb[3 * i + 1], rgb[3 * i + 2], 0.f);
+    // cull helpers: minimiser slope along the other axis, -B/(2C) and -B/(2A)
+    r[1] = make_float4(kp.scale * c, o, thr_m, -b / c);
+    r[2] = make_float4(rgb[3 * i], rgb[3 * i + 1], rgb[3 * i + 2], -b / a);
     r[3] = make_float4(a, b, c, 0.f);
 }
 
 // ------------------------------------------------------------ shared pieces
 
 // Lower bound of m(d) = A dx^2 + B dx dy + C dy^2 over the rectangle of pixel
-// centres [X0,X1]x[Y0,Y1] (d measured from the splat centre).  A, C > 0 and
+// centres [X0,X1]x[Y0,Y1] (d measured from the splat centre), for A, C > 0 and
 // 4AC > B^2 (the pack kernel sends every other conic down the NaN path).  The
 // minimum of a convex quadratic over a box that does not contain the
-// unconstrained minimiser lies on an edge facing it.
+// unconstrained minimiser lies on an edge facing it; evaluated branch-free:
+// candidate 1 = best point of the vertical line through the x-clamped centre,
+// candidate 2 = same for the horizontal line; when the centre is inside the
+// box both are 0, when it is outside along one axis only the candidate of the
+// other axis lies on the facing edge too and is not smaller.
+// kx = -B/(2C), ky = -B/(2A) come precomputed with the record.
 __device__ __forceinline__ bool block_survives(float mx, float my, float A, float B, float C,
-                                               float thr, float band, float X0, float X1,
-                                               float Y0, float Y1) {
-    if (!(thr == thr)) return true;  // NaN threshold: always decided in FP64
-    float ex0 = X0 - mx, ex1 = X1 - mx, ey0 = Y0 - my, ey1 = Y1 - my;
-    bool out_x = (ex0 > 0.f) || (ex1 < 0.f);
-    bool out_y = (ey0 > 0.f) || (ey1 < 0.f);
-    float mmin = 0.f;
-    if (out_x || out_y) {
-        mmin = 3.0e38f;
-        if (out_x) {
-            float dx = ex0 > 0.f ? ex0 : ex1;
-            float dy = __fdividef(-0.5f * B * dx, C);
-            dy = fminf(fmaxf(dy, ey0), ey1);
-            mmin = fmaf(fmaf(A, dx, B * dy), dx, C * dy * dy);
-        }
-        if (out_y) {
-            float dy = ey0 > 0.f ? ey0 : ey1;
-            float dx = __fdividef(-0.5f * B * dy, A);
-            dx = fminf(fmaxf(dx, ex0), ex1);
-            mmin = fminf(mmin, fmaf(fmaf(A, dx, B * dy), dx, C * dy * dy));
-        }
-    }
+                                               float kx, float ky, float thr, float band2,
+                                               float X0, float X1, float Y0, float Y1) {
+    const float ex0 = X0 - mx, ex1 = X1 - mx, ey0 = Y0 - my, ey1 = Y1 - my;
+    const float dxc = fminf(fmaxf(0.f, ex0), ex1);
+    const float dyc = fminf(fmaxf(0.f, ey0), ey1);
+    const float dy1 = fminf(fmaxf(kx * dxc, ey0), ey1);
+    const float m1 = fmaf(fmaf(A, dxc, B * dy1), dxc, (C * dy1) * dy1);
+    const float dx2 = fminf(fmaxf(ky * dyc, ex0), ex1);
+    const float m2 = fmaf(fmaf(A, dx2, B * dyc), dx2, (C * dyc) * dyc);
+    const float mmin = fminf(m1, m2);
     // Per-pixel decisions can only be positive for m <= thr + band; keep a
-    // relative margin for the FP32 rounding of mmin itself.
-    return mmin * 0.9999f <= thr + 2.f * band;
+    // relative margin for the FP32 rounding of mmin itself.  A NaN threshold
+    // (decided in FP64) compares false and survives.
+    return !(mmin * 0.9999f > thr + band2);
 }
 
 // FP32 generic evaluation of eval() for FAM_GENERIC (kernel.cpp:127-164).
@@ -141,18 +136,14 @@ __device__ __forceinline__ void generic_eval(const KParams& kp, float dm2, float
     dw = df * du;
 }
 
-struct Decision {
-    float alpha;  // clamped alpha actually blended
-    float w;      // kernel weight
-    float dwdm;   // d weight / d m
-    bool gate;    // alpha_raw < 0.99: the clamp lets the gradient through (rasterizer.cpp:202)
-};
-
 // The reference's per-visit logic (rasterizer.cpp:90-95 / :181-187) in FP64 on
 // the values the reference would see (the float32 inputs widened), with its
-// expression order (conic_dm2 rasterizer.cpp:19-21).
-__device__ __noinline__ bool exact_decide(const KParams& kp, const float4* __restrict__ recs,
-                                          int idx, float fx, float fy, Decision& out) {
+// expression order (conic_dm2 rasterizer.cpp:19-21).  Returns
+// { clamped alpha, weight, d weight / d m, flags } with flags bit 0 = the visit
+// contributes, bit 1 = alpha_raw < 0.99 (the clamp lets the gradient through,
+// rasterizer.cpp:202).  Out of line: taken for a few visits per million.
+__device__ __noinline__ float4 exact_decide(const KParams& kp, const float4* __restrict__ recs,
+                                            int idx, float fx, float fy) {
     const float4 v0 = __ldg(recs + kRecVecs * (int64_t)idx);
     const float4 v1 = __ldg(recs + kRecVecs * (int64_t)idx + 1);
     const float4 v3 = __ldg(recs + kRecVecs * (int64_t)idx + 3);
@@ -161,176 +152,276 @@ __device__ __noinline__ bool exact_decide(const KParams& kp, const float4* __res
     double dm2 = __dadd_rn(__dadd_rn(__dmul_rn(__dmul_rn(a, dx), dx),
                                      __dmul_rn(__dmul_rn(__dmul_rn(2.0, b), dx), dy)),
                            __dmul_rn(__dmul_rn(c, dy), dy));
-    if (!(dm2 >= 0.0)) return false;  // dm2 < 0 (or NaN, which the reference rejects)
+    float4 out = make_float4(0.f, 0.f, 0.f, __int_as_float(0));
+    if (!(dm2 >= 0.0)) return out;  // dm2 < 0 (or NaN, which the reference rejects)
     double w, dw;
     eval_exact(kp, dm2, w, dw);
     double alpha_raw = o * w;
     double alpha = fmin(kAlphaClampD, alpha_raw);
-    if (alpha < kAlphaSkipD) return false;
-    out.alpha = (float)alpha;
-    out.w = (float)w;
-    out.dwdm = (float)(dw / (double)kp.scale);
-    out.gate = alpha_raw < kAlphaClampD;
-    return true;
+    if (alpha < kAlphaSkipD) return out;
+    out.x = (float)alpha;
+    out.y = (float)w;
+    out.z = (float)(dw / (double)kp.scale);
+    out.w = __int_as_float(1 | (alpha_raw < kAlphaClampD ? 2 : 0));
+    return out;
 }
 
-// One (pixel, entry) visit.  m = scaled squared Mahalanobis distance computed
-// by the caller with a fixed FMA order shared by forward and backward, so both
-// passes take identical decisions.
+// FP32 decision of one (pixel, entry) visit.  m = scaled squared Mahalanobis
+// distance, computed by the caller with a fixed FMA order shared by forward
+// and backward so that both passes take identical decisions.  `near` flags a
+// value inside the guard band of a threshold (re-decided in FP64 when
+// kp.exact); a_raw = opacity * weight, unclamped.
 template <int FAM, bool GRAD>
-__device__ __forceinline__ bool visit(const KParams& kp, const float4* __restrict__ recs, int idx,
-                                      float fx, float fy, float m, float thr, float o,
-                                      Decision& dec, unsigned& nexact) {
-    bool near;
+__device__ __forceinline__ void fast_decide(const KParams& kp, float m, float thr, float o,
+                                            bool& hit, bool& near, float& a_raw, float& w,
+                                            float& dwdm) {
     if constexpr (FAM == FAM_GENERIC) {
         // m == dm2 here (scale 1); thr == cutoff.
         near = !(fabsf(m) > kp.band) || !(fabsf(m - kp.cutoff) > kp.band);
-        if (!near) {
-            if (m < 0.f || m > kp.cutoff) return false;
-            generic_eval(kp, m, dec.w, dec.dwdm);
-            float alpha_raw = o * dec.w;
-            near = !(fabsf(alpha_raw - kAlphaSkipF) > 2e-6f);
-            if (GRAD) near = near || !(fabsf(alpha_raw - kAlphaClampF) > 2e-6f);
-            if (!near || !kp.exact) {
-                dec.alpha = fminf(kAlphaClampF, alpha_raw);
-                dec.gate = alpha_raw < kAlphaClampF;
-                return !(dec.alpha < kAlphaSkipF);
-            }
-        }
-        if (!kp.exact) return false;
+        const bool in_support = !(m < 0.f) && !(m > kp.cutoff);
+        generic_eval(kp, fmaxf(m, 0.f), w, dwdm);
+        a_raw = o * w;
+        near = near || !(fabsf(a_raw - kAlphaSkipF) > 2e-6f);
+        if (GRAD) near = near || !(fabsf(a_raw - kAlphaClampF) > 2e-6f);
+        hit = in_support && !(fminf(kAlphaClampF, a_raw) < kAlphaSkipF);
     } else {
-        float d = thr - m;
+        const float d = thr - m;
         near = !(fabsf(d) > kp.band);  // also true for a NaN threshold
-        if (!near || !kp.exact) {
-            if (!(d > 0.f)) return false;
-            if (GRAD) {
-                fam_eval<FAM>(m, dec.w, dec.dwdm);
-            } else {
-                dec.w = fam_weight<FAM>(m);
-            }
-            float alpha_raw = o * dec.w;
-            dec.alpha = fminf(kAlphaClampF, alpha_raw);
-            dec.gate = alpha_raw < kAlphaClampF;
-            if (!GRAD || !kp.exact || fabsf(alpha_raw - kAlphaClampF) > 2e-6f) return true;
+        hit = d > 0.f;
+        if (GRAD) {
+            fam_eval<FAM>(m, w, dwdm);
+        } else {
+            w = fam_weight<FAM>(m);
+            dwdm = 0.f;
         }
+        a_raw = o * w;
+        if (GRAD) near = near || !(fabsf(a_raw - kAlphaClampF) > 2e-6f);
     }
-    ++nexact;
-    return exact_decide(kp, recs, idx, fx, fy, dec);
 }
 
 __device__ __forceinline__ float quad_m(float A, float B, float C, float dx, float dy) {
     return fmaf(fmaf(A, dx, B * dy), dx, (C * dy) * dy);
 }
 
-struct Chunk {
-    int idx;
+// One list entry as a lane holds it while testing it against the warp's block.
+struct Entry {
     float4 v0, v1, v2;
 };
 
-__device__ __forceinline__ void load_chunk(Chunk& ch, const int* __restrict__ point_list,
-                                           const float4* __restrict__ recs, int k, int end) {
-    if (k < end) {
-        ch.idx = __ldg(point_list + k);
-        const float4* r = recs + kRecVecs * (int64_t)ch.idx;
-        ch.v0 = __ldg(r);
-        ch.v1 = __ldg(r + 1);
-        ch.v2 = __ldg(r + 2);
-    } else {
-        ch.idx = -1;
+__device__ __forceinline__ int load_index(const int* __restrict__ point_list, int k, int lo, int hi) {
+    return (k >= lo && k < hi) ? __ldg(point_list + k) : -1;
+}
+
+__device__ __forceinline__ void load_entry(Entry& e, const float4* __restrict__ recs, int idx) {
+    if (idx >= 0) {
+        const float4* r = recs + kRecVecs * (int64_t)idx;
+        e.v0 = __ldg(r);
+        e.v1 = __ldg(r + 1);
+        e.v2 = __ldg(r + 2);
     }
 }
 
+// Per-warp survivor queue in shared memory: a ring of kQueueCap entries of three
+// float4 { mu.x, mu.y, A, B } { C, opacity, thr_m, list position } { r, g, b,
+// splat index }.  Entries that pass the block test are appended in list order;
+// the compositing loops consume them in fixed-size batches that never wrap.
+constexpr int kQueueCap = 64;
+
+__device__ __forceinline__ void queue_push(float4* q, int slot, const Entry& e, int pos, int idx) {
+    slot &= kQueueCap - 1;
+    q[slot * 3 + 0] = e.v0;
+    q[slot * 3 + 1] = make_float4(e.v1.x, e.v1.y, e.v1.z, __int_as_float(pos));
+    q[slot * 3 + 2] = make_float4(e.v2.x, e.v2.y, e.v2.z, __int_as_float(idx));
+}
+
+// Where the survivor list of block `blk` (0..7, the forward's warp index) of a tile
+// whose point list is [beg, end) starts: every block owns a region as long as the
+// tile's list, the worst case.  8 * K entries of address space; only survivors are
+// ever written or read.
+__device__ __forceinline__ size_t survivor_list_offset(int beg, int end, int blk) {
+    return (size_t)beg * kWarpsPerCta + (size_t)blk * (size_t)(end - beg);
+}
+
 // ------------------------------------------------------------------ forward
+constexpr int kFwdBatch = 32;
+constexpr int kGroup = 8;  // survivors composited speculatively between two guard-band checks
+
+// A pixel is live while its transmittance is at or above the floor
+// (rasterizer.cpp:100 leaves the loop the first time T < 1e-4); lanes outside
+// the image start at T = 0 and never take a splat.
+struct FwdPixel {
+    float T, cr, cg, cb;
+    float contrib;  // contributor count, kept in FP32 (exact below 2^24) so a hit costs one FADD
+    int proc;
+    unsigned nexact;
+};
+
+// Front-to-back compositing of one queued survivor into this lane's pixel
+// (rasterizer.cpp:88-100).  Branch-free: a lane that does not take the splat
+// blends alpha = 0.
+//
+// CAREFUL = false is the speculative form the batch loop runs over a group of
+// survivors: it only records in near_acc whether any FP32 value fell inside
+// the guard band of a threshold; the group is then replayed from the saved
+// pixel state with CAREFUL = true, which re-takes those decisions in FP64.
+template <int FAM, bool CAREFUL>
+__device__ __forceinline__ void fwd_visit(const KParams& kp, const float4* __restrict__ recs,
+                                          const float4* __restrict__ qe, float fx, float fy,
+                                          FwdPixel& px, bool& near_acc) {
+    const float4 s0 = qe[0];
+    const float4 s1 = qe[1];
+    const float4 s2 = qe[2];
+    const float dx = fx - s0.x, dy = fy - s0.y;
+    const float m = quad_m(s0.z, s0.w, s1.x, dx, dy);
+    const bool live = !(px.T < kTFloorF);
+    bool hit, near;
+    float a_raw, w, dwdm;
+    fast_decide<FAM, false>(kp, m, s1.z, s1.y, hit, near, a_raw, w, dwdm);
+    float alpha = fminf(kAlphaClampF, a_raw);
+    if constexpr (CAREFUL) {
+        if (kp.exact && near && live) {
+            const float4 r = exact_decide(kp, recs, __float_as_int(s2.w), fx, fy);
+            hit = __float_as_int(r.w) & 1;
+            alpha = r.x;
+            ++px.nexact;
+        }
+    } else {
+        near_acc = near_acc || near;
+    }
+    const float hitf = (hit && live) ? 1.f : 0.f;
+    alpha *= hitf;
+    // rasterizer.cpp:96-100
+    const float at = alpha * px.T;
+    px.cr = fmaf(s2.x, at, px.cr);
+    px.cg = fmaf(s2.y, at, px.cg);
+    px.cb = fmaf(s2.z, at, px.cb);
+    const float Tn = fmaf(-alpha, px.T, px.T);
+    px.contrib += hitf;
+    // the step that crossed the floor (a live lane that does not take the splat keeps T)
+    if (live && Tn < kTFloorF) px.proc = __float_as_int(s1.w) + 1;
+    px.T = Tn;
+}
+
 template <int FAM>
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(kThreads, 3)
 render_fwd_kernel(KParams kp, const float4* __restrict__ recs, const int2* __restrict__ ranges,
                   const int* __restrict__ point_list, int W, int H, int tiles_x, float bg0,
                   float bg1, float bg2, float* __restrict__ image, float* __restrict__ t_final,
                   int* __restrict__ processed, int* __restrict__ contributors,
+                  int2* __restrict__ surv, int* __restrict__ surv_count,
                   unsigned long long* __restrict__ counters) {
-    __shared__ float4 stage[kWarpsPerCta][32 * 3];
+    __shared__ float4 queue[kWarpsPerCta][kQueueCap * 3];
     const int tile = blockIdx.x;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    // the warp index through a warp reduction: the compiler then knows it is warp-uniform and
+    // keeps the block rectangle, queue pointer and loop control in uniform registers
+    const int warp = __reduce_min_sync(kFull, (int)(threadIdx.x >> 5)), lane = threadIdx.x & 31;
     const int bx = (tile % tiles_x) * DARBS_TILE_SIZE + (warp & 1) * 8;
     const int by = (tile / tiles_x) * DARBS_TILE_SIZE + (warp >> 1) * 4;
     if (bx >= W || by >= H) return;  // whole block outside the image
-    const int px = bx + (lane & 7), py = by + (lane >> 3);
-    const bool inside = px < W && py < H;
-    const float fx = px + 0.5f, fy = py + 0.5f;
+    const int pxl = bx + (lane & 7), pyl = by + (lane >> 3);
+    const bool inside = pxl < W && pyl < H;
+    const float fx = pxl + 0.5f, fy = pyl + 0.5f;
     const float X0 = bx + 0.5f, X1 = bx + 7.5f, Y0 = by + 0.5f, Y1 = by + 3.5f;
     const int2 range = ranges[tile];
     const int beg = range.x, end = range.y;
+    const float band2 = 2.f * kp.band;
 
-    float T = 1.f, cr = 0.f, cg = 0.f, cb = 0.f;
-    int contrib = 0, proc = end - beg;
-    bool active = inside;
-    unsigned nexact = 0, nsurv = 0, nfloor = 0;
-    float4* st = stage[warp];
+    FwdPixel px;
+    px.T = inside ? 1.f : 0.f;
+    px.cr = px.cg = px.cb = 0.f;
+    px.contrib = 0.f;
+    px.proc = end - beg;
+    px.nexact = 0;
+    int nsurv = 0;
+    float4* q = queue[warp];
     const unsigned lt_mask = (1u << lane) - 1u;
+    int head = 0, qn = 0;  // ring: entries [head, head + qn)
+    // this block's survivor list (splat index, list position), kept for the backward pass
+    int2* sl = surv + survivor_list_offset(beg, end, warp);
 
-    Chunk cur, nxt;
-    load_chunk(cur, point_list, recs, beg + lane, end);
+    // software pipeline: indices two chunks ahead, records one chunk ahead
+    int idx_cur = load_index(point_list, beg + lane, beg, end);
+    int idx_nxt = load_index(point_list, beg + 32 + lane, beg, end);
+    Entry cur, nxt;
+    load_entry(cur, recs, idx_cur);
     for (int base = beg; base < end; base += 32) {
-        if (base + 32 < end) load_chunk(nxt, point_list, recs, base + 32 + lane, end);
-        bool survive = cur.idx >= 0 &&
-                       block_survives(cur.v0.x, cur.v0.y, cur.v0.z, cur.v0.w, cur.v1.x, cur.v1.z,
-                                      kp.band, X0, X1, Y0, Y1);
+        load_entry(nxt, recs, idx_nxt);
+        const int idx_nn = load_index(point_list, base + 64 + lane, beg, end);
+        const bool survive =
+            idx_cur >= 0 && block_survives(cur.v0.x, cur.v0.y, cur.v0.z, cur.v0.w, cur.v1.x, cur.v1.w,
+                                           cur.v2.w, cur.v1.z, band2, X0, X1, Y0, Y1);
         const unsigned mask = __ballot_sync(kFull, survive);
+        if (survive) {
+            const int rank = __popc(mask & lt_mask);
+            queue_push(q, head + qn + rank, cur, base - beg + lane, idx_cur);
+            sl[nsurv + rank] = make_int2(idx_cur, base - beg + lane);
+        }
         const int cnt = __popc(mask);
-        if (cnt) {
-            if (survive) {
-                int slot = __popc(mask & lt_mask);
-                st[slot * 3 + 0] = cur.v0;
-                st[slot * 3 + 1] = make_float4(cur.v1.x, cur.v1.y, cur.v1.z,
-                                               __int_as_float(base - beg + lane));
-                st[slot * 3 + 2] = make_float4(cur.v2.x, cur.v2.y, cur.v2.z,
-                                               __int_as_float(cur.idx));
-            }
+        qn += cnt;
+        nsurv += cnt;
+        const bool last = base + 32 >= end;
+        if (qn >= kFwdBatch || (last && qn > 0)) {
             __syncwarp();
-            nsurv += cnt;
-            for (int j = 0; j < cnt; ++j) {
-                const float4 s0 = st[j * 3 + 0];
-                const float4 s1 = st[j * 3 + 1];
-                if (active) {
-                    float dx = fx - s0.x, dy = fy - s0.y;
-                    float m = quad_m(s0.z, s0.w, s1.x, dx, dy);
-                    Decision dec;
-                    const float4 s2 = st[j * 3 + 2];
-                    if (visit<FAM, false>(kp, recs, __float_as_int(s2.w), fx, fy, m, s1.z, s1.y,
-                                          dec, nexact)) {
-                        // rasterizer.cpp:96-100
-                        float at = dec.alpha * T;
-                        cr = fmaf(s2.x, at, cr);
-                        cg = fmaf(s2.y, at, cg);
-                        cb = fmaf(s2.z, at, cb);
-                        T *= 1.0f - dec.alpha;
-                        ++contrib;
-                        if (fabsf(T - kTFloorF) < 2e-9f) ++nfloor;
-                        if (T < kTFloorF) {
-                            active = false;
-                            proc = __float_as_int(s1.w) + 1;
-                        }
+            while (qn >= kFwdBatch) {
+                const float4* qb = q + head * 3;
+                for (int j0 = 0; j0 < kFwdBatch; j0 += kGroup) {
+                    const FwdPixel save = px;
+                    bool near_acc = false;
+#pragma unroll
+                    for (int j = 0; j < kGroup; ++j)
+                        fwd_visit<FAM, false>(kp, recs, qb + (j0 + j) * 3, fx, fy, px, near_acc);
+                    if (kp.exact && __any_sync(kFull, near_acc)) {  // a few groups per thousand
+                        px = save;
+                        for (int j = 0; j < kGroup; ++j)
+                            fwd_visit<FAM, true>(kp, recs, qb + (j0 + j) * 3, fx, fy, px, near_acc);
                     }
                 }
+                head = (head + kFwdBatch) & (kQueueCap - 1);
+                qn -= kFwdBatch;
+            }
+            if (last) {
+                const float4* qb = q + head * 3;
+                bool unused = false;
+                for (int j = 0; j < qn; ++j) fwd_visit<FAM, true>(kp, recs, qb + j * 3, fx, fy, px, unused);
+                qn = 0;
             }
             __syncwarp();
-            if (!__any_sync(kFull, active)) break;
+            if (!__any_sync(kFull, !(px.T < kTFloorF))) break;
         }
         cur = nxt;
+        idx_cur = idx_nxt;
+        idx_nxt = idx_nn;
     }
+    // pixels whose transmittance came within the guard band of the floor: the last value
+    // (the first below the floor, or the final one) and, for a pixel that crossed, the value
+    // just before the crossing, recovered from the splat that crossed it
+    unsigned nfloor = 0;
     if (inside) {
-        size_t p = (size_t)py * W + px;
-        image[p * 3 + 0] = fmaf(bg0, T, cr);
-        image[p * 3 + 1] = fmaf(bg1, T, cg);
-        image[p * 3 + 2] = fmaf(bg2, T, cb);
-        t_final[p] = T;
-        processed[p] = proc;
-        contributors[p] = contrib;
+        nfloor = fabsf(px.T - kTFloorF) < 2e-9f;
+        if (px.T < kTFloorF && px.proc > 0) {
+            const int idx = __ldg(point_list + beg + px.proc - 1);
+            const float4 v0 = __ldg(recs + kRecVecs * (int64_t)idx);
+            const float4 v1 = __ldg(recs + kRecVecs * (int64_t)idx + 1);
+            bool hit, near;
+            float a_raw, w, dwdm;
+            fast_decide<FAM, false>(kp, quad_m(v0.z, v0.w, v1.x, fx - v0.x, fy - v0.y), v1.z, v1.y, hit, near,
+                                    a_raw, w, dwdm);
+            const float t_cross = px.T / (1.0f - fminf(kAlphaClampF, a_raw));
+            nfloor = nfloor || fabsf(t_cross - kTFloorF) < 4e-9f;
+        }
+        size_t p = (size_t)pyl * W + pxl;
+        image[p * 3 + 0] = fmaf(bg0, px.T, px.cr);
+        image[p * 3 + 1] = fmaf(bg1, px.T, px.cg);
+        image[p * 3 + 2] = fmaf(bg2, px.T, px.cb);
+        t_final[p] = px.T;
+        processed[p] = px.proc;
+        contributors[p] = (int)px.contrib;
     }
     // instrumentation: one atomic per warp per counter
-    nexact = __reduce_add_sync(kFull, nexact);
+    const unsigned nexact = __reduce_add_sync(kFull, px.nexact);
     nfloor = __reduce_add_sync(kFull, nfloor);
     if (lane == 0) {
+        surv_count[tile * kWarpsPerCta + warp] = nsurv;
         atomicAdd(counters + CNT_SURVIVORS, (unsigned long long)nsurv);
         if (nexact) atomicAdd(counters + CNT_EXACT, (unsigned long long)nexact);
         if (nfloor) atomicAdd(counters + CNT_TFLOOR, (unsigned long long)nfloor);
@@ -338,156 +429,248 @@ render_fwd_kernel(KParams kp, const float4* __restrict__ recs, const int2* __res
 }
 
 // ----------------------------------------------------------------- backward
+//
+// One CTA of 4 warps per HALF tile (16x8 pixels); a warp owns an 8x4 block as in
+// the forward.  The list is walked back to front in two sweeps per batch of
+// kBwdBatch queued survivors:
+//   sweep 1 (lane = pixel): the reverse compositing chain of rasterizer.cpp:
+//       189-213; per (pixel, survivor) it leaves three numbers in a padded
+//       shared-memory matrix: wgt = alpha * T_before (colour gradient weight),
+//       y = d_alpha * w (opacity gradient term), z = d_alpha * o * dw/dm (the
+//       common factor of the conic and mean gradients), the last two gated by
+//       the alpha clamp;
+//   sweep 2 (lane = survivor x half of the pixels): each lane sums its
+//       survivor's nine gradients over 16 pixels in registers; one shuffle
+//       folds the two halves.  No per-survivor cross-lane reduction.
+// Then one red.global.add per gradient component per survivor.
+constexpr int kBwdWarps = 4;
+constexpr int kBwdThreads = 32 * kBwdWarps;
+constexpr int kBwdBatch = 16;
+constexpr int kXStride = kBwdBatch + 1;  // odd: conflict-free both by row and by column
 
-// Sum over the warp of 9 per-lane values; afterwards lanes 0,4,..,28 hold
-// v[0..7] (lane >> 2) and every lane holds v[8] in `e`.  Reduce-scatter
-// butterfly: 4+2+1 exchanges split the 8 values across lane bits 4,3,2, two
-// more finish them; 14 shuffles instead of 45.
-__device__ __forceinline__ float warp_reduce9(float (&v)[8], float& e, int lane) {
-    const bool h16 = lane & 16, h8 = lane & 8, h4 = lane & 4;
-    float u[4];
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-        float keep = h16 ? v[i + 4] : v[i];
-        float send = h16 ? v[i] : v[i + 4];
-        u[i] = keep + __shfl_xor_sync(kFull, send, 16);
+struct BwdPixel {
+    float T;       // transmittance in front of the cursor
+    float s;       // <g, colour composited behind the cursor> (rasterizer.cpp:180)
+    float g0, g1, g2;
+    int nproc;
+    unsigned nexact;
+};
+
+template <int FAM, bool CAREFUL>
+__device__ __forceinline__ void bwd_visit(const KParams& kp, const float4* __restrict__ recs,
+                                          const float4* __restrict__ qe, float fx, float fy,
+                                          BwdPixel& px, float* __restrict__ xw,
+                                          float* __restrict__ xy, float* __restrict__ xz,
+                                          bool& near_acc) {
+    const float4 s0 = qe[0];
+    const float4 s1 = qe[1];
+    const float4 s2 = qe[2];
+    const float dx = fx - s0.x, dy = fy - s0.y;
+    const float m = quad_m(s0.z, s0.w, s1.x, dx, dy);
+    const bool elig = __float_as_int(s1.w) < px.nproc;
+    bool hit, near;
+    float a_raw, w, dwdm;
+    fast_decide<FAM, true>(kp, m, s1.z, s1.y, hit, near, a_raw, w, dwdm);
+    float alpha = fminf(kAlphaClampF, a_raw);
+    bool gate = a_raw < kAlphaClampF;
+    if constexpr (CAREFUL) {
+        if (kp.exact && near && elig) {
+            const float4 r = exact_decide(kp, recs, __float_as_int(s2.w), fx, fy);
+            const int flags = __float_as_int(r.w);
+            hit = flags & 1;
+            gate = flags & 2;
+            alpha = r.x;
+            w = r.y;
+            dwdm = r.z;
+            ++px.nexact;
+        }
+    } else {
+        near_acc = near_acc || near;
     }
-    float t[2];
-#pragma unroll
-    for (int i = 0; i < 2; ++i) {
-        float keep = h8 ? u[i + 2] : u[i];
-        float send = h8 ? u[i] : u[i + 2];
-        t[i] = keep + __shfl_xor_sync(kFull, send, 8);
-    }
-    float keep = h4 ? t[1] : t[0];
-    float send = h4 ? t[0] : t[1];
-    float s = keep + __shfl_xor_sync(kFull, send, 4);
-    s += __shfl_xor_sync(kFull, s, 2);
-    s += __shfl_xor_sync(kFull, s, 1);
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) e += __shfl_xor_sync(kFull, e, o);
-    return s;  // value index (lane >> 2) & 7 ... see caller
+    hit = hit && elig;
+    gate = gate && hit;
+    alpha = hit ? alpha : 0.f;
+    // rasterizer.cpp:189-213 with s = <g, accum_behind>
+    const float om = 1.0f - alpha;
+    const float rc = rcp_approx(om);
+    const float t_before = px.T * rc;
+    const float wgt = alpha * t_before;
+    const float gc = fmaf(px.g2, s2.z, fmaf(px.g1, s2.y, px.g0 * s2.x));
+    const float d_alpha = fmaf(t_before, gc, -(rc * px.s));
+    const float da = gate ? d_alpha : 0.f;
+    *xw = wgt;
+    *xy = da * w;
+    *xz = da * s1.y * dwdm;
+    px.s = fmaf(gc, wgt, px.s);
+    if (hit) px.T = t_before;
 }
 
 template <int FAM>
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(kBwdThreads)
 render_bwd_kernel(KParams kp, const float4* __restrict__ recs, const int2* __restrict__ ranges,
-                  const int* __restrict__ point_list, int W, int H, int tiles_x, float bg0,
-                  float bg1, float bg2, const float* __restrict__ grad_image,
+                  const int2* __restrict__ surv, const int* __restrict__ surv_count, int W, int H,
+                  int tiles_x, float bg0, float bg1, float bg2, const float* __restrict__ grad_image,
                   const float* __restrict__ t_final, const int* __restrict__ processed,
                   float* __restrict__ grads, unsigned long long* __restrict__ counters) {
-    __shared__ float4 stage[kWarpsPerCta][32 * 3];
-    const int tile = blockIdx.x;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    __shared__ float4 queue[kBwdWarps][kQueueCap * 3];
+    __shared__ float xch[kBwdWarps][3][32 * kXStride];
+    __shared__ float4 gpix[kBwdWarps][32];
+    const int tile = blockIdx.x >> 1, half = blockIdx.x & 1;
+    const int warp = __reduce_min_sync(kFull, (int)(threadIdx.x >> 5)), lane = threadIdx.x & 31;
+    const int blk = half * kBwdWarps + warp;  // the forward's warp index of this block
     const int bx = (tile % tiles_x) * DARBS_TILE_SIZE + (warp & 1) * 8;
-    const int by = (tile / tiles_x) * DARBS_TILE_SIZE + (warp >> 1) * 4;
+    const int by = (tile / tiles_x) * DARBS_TILE_SIZE + half * 8 + (warp >> 1) * 4;
     if (bx >= W || by >= H) return;
-    const int px = bx + (lane & 7), py = by + (lane >> 3);
-    const bool inside = px < W && py < H;
-    const float fx = px + 0.5f, fy = py + 0.5f;
-    const float X0 = bx + 0.5f, X1 = bx + 7.5f, Y0 = by + 0.5f, Y1 = by + 3.5f;
-    const int beg = ranges[tile].x;
+    const int pxl = bx + (lane & 7), pyl = by + (lane >> 3);
+    const bool inside = pxl < W && pyl < H;
+    const float fx = pxl + 0.5f, fy = pyl + 0.5f;
+    const float X0 = bx + 0.5f, Y0 = by + 0.5f;
+    const int2 range = ranges[tile];
 
-    float g0 = 0.f, g1 = 0.f, g2 = 0.f, T = 1.f;
-    int nproc = 0;
+    BwdPixel px;
+    px.g0 = px.g1 = px.g2 = 0.f;
+    px.T = 1.f;
+    px.nproc = 0;
+    px.nexact = 0;
     if (inside) {
-        size_t p = (size_t)py * W + px;
-        g0 = grad_image[p * 3 + 0];
-        g1 = grad_image[p * 3 + 1];
-        g2 = grad_image[p * 3 + 2];
-        T = t_final[p];
-        nproc = processed[p];
+        size_t p = (size_t)pyl * W + pxl;
+        px.g0 = grad_image[p * 3 + 0];
+        px.g1 = grad_image[p * 3 + 1];
+        px.g2 = grad_image[p * 3 + 2];
+        px.T = t_final[p];
+        px.nproc = processed[p];
     }
-    const int wmax = __reduce_max_sync(kFull, nproc);
+    const int wmax = __reduce_max_sync(kFull, px.nproc);
     if (wmax == 0) return;
-    const int end = beg + wmax;
-    // colour composited behind the cursor (rasterizer.cpp:180)
-    float b0 = bg0 * T, b1 = bg1 * T, b2 = bg2 * T;
+    px.s = (px.g0 * bg0 + px.g1 * bg1 + px.g2 * bg2) * px.T;
 
-    // which of the 8 scatter-reduced values this lane owns, and its unscaling:
-    // SplatGrads order d_color[3], d_opacity, d_conic_a, d_conic_b, d_conic_c, d_mu2.x
-    // with m = scale*(a dx^2 + 2b dx dy + c dy^2): d/da = scale*dx^2, d/db = 2*scale*dx*dy.
-    const int vi = ((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1);
-    const float vmul = (vi == 4 || vi == 6) ? kp.scale : (vi == 5 ? 2.f * kp.scale : 1.f);
-    const bool owner = (lane & 3) == 0;
+    float4* q = queue[warp];
+    float* xw = xch[warp][0];
+    float* xy = xch[warp][1];
+    float* xz = xch[warp][2];
+    gpix[warp][lane] = make_float4(px.g0, px.g1, px.g2, 0.f);
+    const unsigned lt_mask = (1u << lane) - 1u;
+    int head = 0, qn = 0;
 
-    unsigned nexact = 0;
-    float4* st = stage[warp];
-    const unsigned gt_mask = lane == 31 ? 0u : ~((2u << lane) - 1u);
+    // sweep-2 role of this lane: survivor sj of the batch, pixels [16 sh, 16 sh + 16)
+    const int sj = lane & (kBwdBatch - 1), sh = lane >> 4;
+    const float* rw = xw + (sh * 16) * kXStride + sj;
+    const float* ry = xy + (sh * 16) * kXStride + sj;
+    const float* rz = xz + (sh * 16) * kXStride + sj;
+    const float4* rg = gpix[warp] + sh * 16;
+    const float ex0 = X0, ey0 = Y0 + 2.f * sh;
 
-    const int nchunks = (wmax + 31) >> 5;
-    Chunk cur, nxt;
-    load_chunk(cur, point_list, recs, beg + (nchunks - 1) * 32 + lane, end);
-    for (int ch = nchunks - 1; ch >= 0; --ch) {
-        const int base = beg + ch * 32;
-        if (ch > 0) load_chunk(nxt, point_list, recs, base - 32 + lane, end);
-        bool survive = cur.idx >= 0 &&
-                       block_survives(cur.v0.x, cur.v0.y, cur.v0.z, cur.v0.w, cur.v1.x, cur.v1.z,
-                                      kp.band, X0, X1, Y0, Y1);
+    // The block's survivors, as the forward queued them, walked from the back: lane l of a
+    // chunk takes the l-th entry from the chunk's end, so lane order is descending list
+    // position.  Entries the forward queued beyond the last position any of this block's
+    // pixels processed (at most a batch and a half) are dropped here.
+    const int2* sl = surv + survivor_list_offset(range.x, range.y, blk);
+    const int nsl = surv_count[tile * kWarpsPerCta + blk];
+    auto load_ref = [&](int k) { return k >= 0 ? __ldg(sl + k) : make_int2(-1, 0); };
+    int2 ref_cur = load_ref(nsl - 1 - lane);
+    int2 ref_nxt = load_ref(nsl - 33 - lane);
+    Entry cur, nxt;
+    load_entry(cur, recs, ref_cur.x);
+    for (int top = nsl; top > 0; top -= 32) {
+        load_entry(nxt, recs, ref_nxt.x);
+        const int2 ref_nn = load_ref(top - 65 - lane);
+        const bool survive = ref_cur.x >= 0 && ref_cur.y < wmax;
         const unsigned mask = __ballot_sync(kFull, survive);
-        const int cnt = __popc(mask);
-        if (cnt) {
-            if (survive) {
-                int slot = __popc(mask & gt_mask);  // descending list position
-                st[slot * 3 + 0] = cur.v0;
-                st[slot * 3 + 1] = make_float4(cur.v1.x, cur.v1.y, cur.v1.z,
-                                               __int_as_float(base - beg + lane));
-                st[slot * 3 + 2] = make_float4(cur.v2.x, cur.v2.y, cur.v2.z,
-                                               __int_as_float(cur.idx));
-            }
+        if (survive) queue_push(q, head + qn + __popc(mask & lt_mask), cur, ref_cur.y, ref_cur.x);
+        qn += __popc(mask);
+        const bool last = top <= 32;
+        while (qn >= kBwdBatch || (last && qn > 0)) {
+            const int n = qn < kBwdBatch ? qn : kBwdBatch;
+            const float4* qb = q + head * 3;
             __syncwarp();
-            for (int j = 0; j < cnt; ++j) {
-                const float4 s0 = st[j * 3 + 0];
-                const float4 s1 = st[j * 3 + 1];
-                const float4 s2 = st[j * 3 + 2];
-                const int idx = __float_as_int(s2.w);
-                float v[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-                float e = 0.f;
-                bool hit = false;
-                if (__float_as_int(s1.w) < nproc) {
-                    float dx = fx - s0.x, dy = fy - s0.y;
-                    float m = quad_m(s0.z, s0.w, s1.x, dx, dy);
-                    Decision dec;
-                    hit = visit<FAM, true>(kp, recs, idx, fx, fy, m, s1.z, s1.y, dec, nexact);
-                    if (hit) {
-                        // rasterizer.cpp:189-213
-                        float om = 1.0f - dec.alpha;
-                        float rc = __frcp_rn(om);
-                        float t_before = T * rc;
-                        float wgt = dec.alpha * t_before;
-                        v[0] = g0 * wgt;
-                        v[1] = g1 * wgt;
-                        v[2] = g2 * wgt;
-                        float d_alpha = g0 * fmaf(s2.x, t_before, -b0 * rc) +
-                                        g1 * fmaf(s2.y, t_before, -b1 * rc) +
-                                        g2 * fmaf(s2.z, t_before, -b2 * rc);
-                        if (dec.gate) {
-                            v[3] = d_alpha * dec.w;
-                            float d_m = d_alpha * s1.y * dec.dwdm;
-                            v[4] = d_m * dx * dx;
-                            v[5] = d_m * dx * dy;
-                            v[6] = d_m * dy * dy;
-                            v[7] = -d_m * fmaf(2.f * s0.z, dx, s0.w * dy);
-                            e = -d_m * fmaf(s0.w, dx, 2.f * s1.x * dy);
-                        }
-                        b0 = fmaf(s2.x, wgt, b0);
-                        b1 = fmaf(s2.y, wgt, b1);
-                        b2 = fmaf(s2.z, wgt, b2);
-                        T = t_before;
+            // ---- sweep 1: lane = pixel
+            float* ww = xw + lane * kXStride;
+            float* wy = xy + lane * kXStride;
+            float* wz = xz + lane * kXStride;
+            bool near_acc = false;
+            if (n == kBwdBatch) {
+                for (int j0 = 0; j0 < kBwdBatch; j0 += kGroup) {
+                    const BwdPixel save = px;
+                    near_acc = false;
+#pragma unroll
+                    for (int j = 0; j < kGroup; ++j)
+                        bwd_visit<FAM, false>(kp, recs, qb + (j0 + j) * 3, fx, fy, px, ww + j0 + j, wy + j0 + j,
+                                              wz + j0 + j, near_acc);
+                    if (kp.exact && __any_sync(kFull, near_acc)) {  // a few groups per thousand
+                        px = save;
+                        for (int j = 0; j < kGroup; ++j)
+                            bwd_visit<FAM, true>(kp, recs, qb + (j0 + j) * 3, fx, fy, px, ww + j0 + j, wy + j0 + j,
+                                                 wz + j0 + j, near_acc);
                     }
                 }
-                if (__any_sync(kFull, hit)) {
-                    float s = warp_reduce9(v, e, lane);
-                    float* dst = grads + (size_t)idx * DARBS_GRADS_PER_SPLAT;
-                    if (owner) atomicAdd(dst + vi, s * vmul);
-                    if (lane == 1) atomicAdd(dst + 8, e);
-                }
+            } else {
+                for (int j = 0; j < n; ++j)
+                    bwd_visit<FAM, true>(kp, recs, qb + j * 3, fx, fy, px, ww + j, wy + j, wz + j, near_acc);
             }
             __syncwarp();
+            // ---- sweep 2: lane = (survivor, half of the pixels)
+            if (sj < n) {
+                const float4 r0 = qb[sj * 3 + 0];
+                const float4 r1 = qb[sj * 3 + 1];
+                const float4 r2 = qb[sj * 3 + 2];
+                const float ex = ex0 - r0.x, ey = ey0 - r0.y;
+                float dc0 = 0.f, dc1 = 0.f, dc2 = 0.f, dop = 0.f, wsum = 0.f;
+                float sxx = 0.f, sxy = 0.f, syy = 0.f, sx = 0.f, sy = 0.f;
+#pragma unroll
+                for (int i = 0; i < 16; ++i) {
+                    const float wv = rw[i * kXStride];
+                    const float yv = ry[i * kXStride];
+                    const float zv = rz[i * kXStride];
+                    const float4 g = rg[i];
+                    const float dx = ex + (float)(i & 7), dy = ey + (float)(i >> 3);
+                    dc0 = fmaf(g.x, wv, dc0);
+                    dc1 = fmaf(g.y, wv, dc1);
+                    dc2 = fmaf(g.z, wv, dc2);
+                    wsum += wv;
+                    dop += yv;
+                    const float zx = zv * dx, zy = zv * dy;
+                    sxx = fmaf(zx, dx, sxx);
+                    sxy = fmaf(zx, dy, sxy);
+                    syy = fmaf(zy, dy, syy);
+                    sx += zx;
+                    sy += zy;
+                }
+                // fold the two pixel halves (lanes l and l ^ 16 hold the same survivor)
+                const unsigned pm = n >= kBwdBatch ? kFull : ((1u << n) - 1u) * 0x10001u;
+                dc0 += __shfl_xor_sync(pm, dc0, 16);
+                dc1 += __shfl_xor_sync(pm, dc1, 16);
+                dc2 += __shfl_xor_sync(pm, dc2, 16);
+                dop += __shfl_xor_sync(pm, dop, 16);
+                wsum += __shfl_xor_sync(pm, wsum, 16);
+                sxx += __shfl_xor_sync(pm, sxx, 16);
+                sxy += __shfl_xor_sync(pm, sxy, 16);
+                syy += __shfl_xor_sync(pm, syy, 16);
+                sx += __shfl_xor_sync(pm, sx, 16);
+                sy += __shfl_xor_sync(pm, sy, 16);
+                if (sh == 0 && wsum > 0.f) {
+                    // SplatGrads order d_color[3], d_opacity, d_conic_a, d_conic_b, d_conic_c, d_mu2;
+                    // m = scale * (a dx^2 + 2 b dx dy + c dy^2): dm/da = scale dx^2, dm/db = 2 scale dx dy,
+                    // dm/d mu = -(2A dx + B dy, B dx + 2C dy) with (A, B, C) the scaled record values.
+                    float* dst = grads + (size_t)__float_as_int(r2.w) * DARBS_GRADS_PER_SPLAT;
+                    atomicAdd(dst + 0, dc0);
+                    atomicAdd(dst + 1, dc1);
+                    atomicAdd(dst + 2, dc2);
+                    atomicAdd(dst + 3, dop);
+                    atomicAdd(dst + 4, kp.scale * sxx);
+                    atomicAdd(dst + 5, 2.f * kp.scale * sxy);
+                    atomicAdd(dst + 6, kp.scale * syy);
+                    atomicAdd(dst + 7, -fmaf(2.f * r0.z, sx, r0.w * sy));
+                    atomicAdd(dst + 8, -fmaf(r0.w, sx, 2.f * r1.x * sy));
+                }
+            }
+            head = (head + n) & (kQueueCap - 1);
+            qn -= n;
         }
         cur = nxt;
+        ref_cur = ref_nxt;
+        ref_nxt = ref_nn;
     }
-    nexact = __reduce_add_sync(kFull, nexact);
+    const unsigned nexact = __reduce_add_sync(kFull, px.nexact);
     if (lane == 0 && nexact) atomicAdd(counters + CNT_EXACT, (unsigned long long)nexact);
 }
 
@@ -567,6 +750,11 @@ darbs_status launch_render_fwd(darbs_cuda_ctx* ctx, const KParams& kp, int width
                                int32_t* processed, int32_t* contributors) {
     int tiles = ctx->tiles_x * ctx->tiles_y;
     if (tiles == 0) return DARBS_OK;
+    // per-block survivor lists for the backward pass: 8 regions per tile, each as long as the
+    // tile's list (address space only; the forward writes survivors, a quarter of it or less)
+    const size_t k = (size_t)(ctx->fwd_entries > 0 ? ctx->fwd_entries : 1);
+    DARBS_TRY(reserve(ctx, ctx->surv, sizeof(int2) * kWarpsPerCta * k));
+    DARBS_TRY(reserve(ctx, ctx->surv_count, sizeof(int) * kWarpsPerCta * (size_t)tiles));
     auto* counters = (unsigned long long*)ctx->counters.ptr;
     const float4* recs = (const float4*)ctx->recs.ptr;
     const int2* ranges = (const int2*)ctx->ranges.ptr;
@@ -574,7 +762,7 @@ darbs_status launch_render_fwd(darbs_cuda_ctx* ctx, const KParams& kp, int width
 #define DARBS_LAUNCH_FWD(F)                                                                     \
     render_fwd_kernel<F><<<tiles, kThreads, 0, ctx->stream>>>(                                  \
         kp, recs, ranges, plist, width, height, ctx->tiles_x, bg[0], bg[1], bg[2], image,       \
-        t_final, processed, contributors, counters)
+        t_final, processed, contributors, (int2*)ctx->surv.ptr, (int*)ctx->surv_count.ptr, counters)
     switch (kp.fam) {
         case FAM_GAUSS2: DARBS_LAUNCH_FWD(FAM_GAUSS2); break;
         case FAM_HCOS2: DARBS_LAUNCH_FWD(FAM_HCOS2); break;
@@ -596,11 +784,10 @@ darbs_status launch_render_bwd(darbs_cuda_ctx* ctx, const KParams& kp, int width
     auto* counters = (unsigned long long*)ctx->counters.ptr;
     const float4* recs = (const float4*)ctx->recs.ptr;
     const int2* ranges = (const int2*)ctx->ranges.ptr;
-    const int* plist = point_list_ptr(ctx);
 #define DARBS_LAUNCH_BWD(F)                                                                    \
-    render_bwd_kernel<F><<<tiles, kThreads, 0, ctx->stream>>>(                                 \
-        kp, recs, ranges, plist, width, height, ctx->tiles_x, bg[0], bg[1], bg[2], grad_image, \
-        t_final, processed, grads, counters)
+    render_bwd_kernel<F><<<2 * tiles, kBwdThreads, 0, ctx->stream>>>(                                \
+        kp, recs, ranges, (const int2*)ctx->surv.ptr, (const int*)ctx->surv_count.ptr, width, height,   \
+        ctx->tiles_x, bg[0], bg[1], bg[2], grad_image, t_final, processed, grads, counters)
     switch (kp.fam) {
         case FAM_GAUSS2: DARBS_LAUNCH_BWD(FAM_GAUSS2); break;
         case FAM_HCOS2: DARBS_LAUNCH_BWD(FAM_HCOS2); break;

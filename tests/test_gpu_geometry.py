@@ -191,7 +191,8 @@ def test_evaluate_view_matches_oracle_chain(ctx, port, darbs, name):
     # accumulation over views is a plain += (fit3d.cpp:148-158)
     pg2 = pg.copy()
     ctx.evaluate_view(gk, psi, raw, DEMO_CAMERA, (0, 0, 0), grad_image=gimg, param_grads=pg2)
-    assert rel_err(pg2, 2.0 * pg.astype(np.float64), 1e-4).max() <= 1e-3
+    # (two launches of an atomically accumulated sum: equal up to float32 summation order)
+    assert rel_err(pg2, 2.0 * pg.astype(np.float64), 1e-4 * max(1.0, np.abs(ref).max())).max() <= 1e-3
 
 
 def test_evaluate_view_l1_loss_and_errors(ctx, port, darbs):
