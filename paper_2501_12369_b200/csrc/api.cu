@@ -236,6 +236,7 @@ darbs_status forward_device(darbs_cuda_ctx* ctx, const KParams& kp, int64_t n, c
         StageScope ts(ctx, ST_BINNING);
         DARBS_TRY(run_binning(ctx, n, mu2, conic, radius, depth, valid, width, height));
         DARBS_TRY(launch_pack(ctx, kp, n, mu2, conic, opacity, rgb));
+        DARBS_TRY(launch_gather(ctx));
     }
     DARBS_TRY(reserve(ctx, ctx->t_final, sizeof(float) * (px ? px : 1)));
     DARBS_TRY(reserve(ctx, ctx->processed, sizeof(int32_t) * (px ? px : 1)));
@@ -315,7 +316,7 @@ void darbs_cuda_destroy(darbs_cuda_ctx* ctx) {
     DeviceGuard guard(ctx->device);
     cudaStreamSynchronize(ctx->stream);
     DeviceBuffer* bufs[] = {&ctx->recs, &ctx->rects, &ctx->depth_keys, &ctx->order, &ctx->offsets,
-                            &ctx->tile_keys, &ctx->tile_vals, &ctx->ranges, &ctx->surv, &ctx->surv_count, &ctx->cub_temp,
+                            &ctx->tile_keys, &ctx->tile_vals, &ctx->ranges, &ctx->stream_recs, &ctx->surv, &ctx->surv_count, &ctx->cub_temp,
                             &ctx->counters, &ctx->t_final, &ctx->processed, &ctx->contributors,
                             &ctx->image, &ctx->valid, &ctx->splat_grads, &ctx->grad_image};
     for (DeviceBuffer* b : bufs)
@@ -544,9 +545,9 @@ darbs_status darbs_cuda_backward(darbs_cuda_ctx* ctx, const darbs_kernel_spec* k
     {
         StageScope ts(ctx, ST_RENDER_BWD);
         DARBS_TRY(launch_render_bwd(ctx, kp, grad_width, grad_height, ctx->fwd_bg, d_gimg,
-                                    (const float*)ctx->t_final.ptr, (const int32_t*)ctx->processed.ptr,
-                                    n, d_grads));
+                                    (const float*)ctx->t_final.ptr, (const int32_t*)ctx->processed.ptr, n));
     }
+    DARBS_TRY(launch_export_grads(ctx, n, d_grads));
     return st.finish();
 }
 
@@ -701,12 +702,10 @@ darbs_status darbs_cuda_evaluate_view(darbs_cuda_ctx* ctx, const darbs_kernel_sp
         d_gimg = (const float*)ctx->grad_image.ptr;
     }
     if (param_grads) {
-        DARBS_TRY(reserve(ctx, ctx->splat_grads, sizeof(float) * DARBS_GRADS_PER_SPLAT * nn));
         {
             StageScope ts(ctx, ST_RENDER_BWD);
             DARBS_TRY(launch_render_bwd(ctx, kp, width, height, background, d_gimg,
-                                        (const float*)ctx->t_final.ptr, (const int32_t*)ctx->processed.ptr,
-                                        n, (float*)ctx->splat_grads.ptr));
+                                        (const float*)ctx->t_final.ptr, (const int32_t*)ctx->processed.ptr, n));
         }
         {
             StageScope ts(ctx, ST_PREPROCESS_BWD);

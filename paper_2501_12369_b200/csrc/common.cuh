@@ -81,15 +81,17 @@ struct darbs_cuda_ctx {
     darbs_b200::DeviceBuffer tile_keys;    // 2 * K u32
     darbs_b200::DeviceBuffer tile_vals;    // 2 * K u32
     darbs_b200::DeviceBuffer ranges;       // tiles * int2
-    darbs_b200::DeviceBuffer surv;         // 8 * K int2 (splat index, list position) per-block survivor lists
+    darbs_b200::DeviceBuffer stream_recs;  // 3 * K float4: records in list order (v0 | v1 | v2)
+    darbs_b200::DeviceBuffer surv;         // 3 * 8K float4: per-block survivor streams (v0 | v1 | v2)
     darbs_b200::DeviceBuffer surv_count;   // 8 * tiles int
+    int64_t surv_stride = 0;               // 8K, the length of one of the three survivor arrays
     darbs_b200::DeviceBuffer cub_temp;
     darbs_b200::DeviceBuffer counters;     // Counters + scalars
     darbs_b200::DeviceBuffer t_final, processed, contributors, image;  // per-pixel aux
     darbs_b200::DeviceBuffer stage_in[8];  // staging for DARBS_HOST calls / internal SoA
     darbs_b200::DeviceBuffer stage_out[8];
     darbs_b200::DeviceBuffer valid;        // per-primitive visibility (evaluate_view)
-    darbs_b200::DeviceBuffer splat_grads;  // 9n
+    darbs_b200::DeviceBuffer splat_grads;  // 12n: SplatGrads rows padded to 12 floats
     darbs_b200::DeviceBuffer grad_image;   // 3wh
     void* pinned = nullptr;                // small pinned host scratch
     size_t pinned_bytes = 0;
@@ -140,9 +142,12 @@ darbs_status launch_pack(darbs_cuda_ctx* ctx, const KParams& kp, int64_t n, cons
 darbs_status launch_render_fwd(darbs_cuda_ctx* ctx, const KParams& kp, int width, int height,
                                const float bg[3], float* image, float* t_final,
                                int32_t* processed, int32_t* contributors);
+darbs_status launch_gather(darbs_cuda_ctx* ctx);
 darbs_status launch_render_bwd(darbs_cuda_ctx* ctx, const KParams& kp, int width, int height,
                                const float bg[3], const float* grad_image, const float* t_final,
-                               const int32_t* processed, int64_t n, float* grads);
+                               const int32_t* processed, int64_t n);
+darbs_status launch_export_grads(darbs_cuda_ctx* ctx, int64_t n, float* out);
+static constexpr int kSplatGradRow = 12;  // floats per row of ctx->splat_grads
 darbs_status launch_eval(darbs_cuda_ctx* ctx, const KParams& kp, int64_t n, const float* dm2,
                          float* w, float* dw, int exact);
 darbs_status launch_sum_counts(darbs_cuda_ctx* ctx, int64_t px, const int32_t* processed,

@@ -339,7 +339,7 @@ __global__ void param_grads_kernel(double psi, int64_t n, const float* __restric
     load_prim(raw + 14 * i, true, p);
     Projected pr;
     if (!project_core(p, cam, psi, DARBS_DILATION, pr)) return;
-    const float* gi = splat_grads + DARBS_GRADS_PER_SPLAT * i;
+    const float* gi = splat_grads + kSplatGradRow * i;  // padded rows, SplatGrads order in the first nine
     double a = pr.cov[0], b = pr.cov[1], c = pr.cov[2];
     double det = a * c - b * b;
     double ca = c / det, cb = -b / det, cc = a / det;  // conic, geometry.cpp:61

@@ -59,6 +59,17 @@ __global__ void pack_kernel(KParams kp, int64_t n, const float* __restrict__ mu2
     r[3] = make_float4(a, b, c, 0.f);
 }
 
+__global__ void gather_kernel(int64_t k, const int* __restrict__ point_list,
+                              const float4* __restrict__ recs, float4* __restrict__ stream) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= k) return;
+    const float4* r = recs + kRecVecs * (int64_t)__ldg(point_list + i);
+    const float4 v0 = __ldg(r), v1 = __ldg(r + 1), v2 = __ldg(r + 2);
+    stream[i] = v0;
+    stream[k + i] = v1;
+    stream[2 * k + i] = v2;
+}
+
 // ------------------------------------------------------------ shared pieces
 
 // Lower bound of m(d) = A dx^2 + B dx dy + C dy^2 over the rectangle of pixel
@@ -208,30 +219,51 @@ struct Entry {
     float4 v0, v1, v2;
 };
 
-__device__ __forceinline__ int load_index(const int* __restrict__ point_list, int k, int lo, int hi) {
-    return (k >= lo && k < hi) ? __ldg(point_list + k) : -1;
-}
-
-__device__ __forceinline__ void load_entry(Entry& e, const float4* __restrict__ recs, int idx) {
-    if (idx >= 0) {
-        const float4* r = recs + kRecVecs * (int64_t)idx;
-        e.v0 = __ldg(r);
-        e.v1 = __ldg(r + 1);
-        e.v2 = __ldg(r + 2);
+// ---- tile-ordered record streams
+// After the sort, gather_kernel copies the three hot vectors of every list
+// entry's record into three arrays in LIST order (v0 | v1 | v2, each K float4),
+// so that the 8 warps of a tile read their entries with fully coalesced loads
+// (4 L1 wavefronts per load instead of one per lane for a gather through the
+// point list) and without a dependent index load.
+__device__ __forceinline__ void load_entry(Entry& e, int& idx, const float4* __restrict__ stream,
+                                           size_t stride, const int* __restrict__ point_list, int k,
+                                           int end) {
+    if (k < end) {
+        e.v0 = __ldg(stream + k);
+        e.v1 = __ldg(stream + stride + k);
+        e.v2 = __ldg(stream + 2 * stride + k);
+        idx = __ldg(point_list + k);
     }
 }
 
-// Per-warp survivor queue in shared memory: a ring of kQueueCap entries of three
+// Per-warp survivor queue in shared memory: a ring of CAP entries of three
 // float4 { mu.x, mu.y, A, B } { C, opacity, thr_m, list position } { r, g, b,
 // splat index }.  Entries that pass the block test are appended in list order;
-// the compositing loops consume them in fixed-size batches that never wrap.
-constexpr int kQueueCap = 64;
-
+// the compositing loops consume them in fixed-size groups that never wrap (CAP
+// is a multiple of the group size): one chunk is appended between two drains,
+// on top of less than one group left over.
+template <int CAP>
 __device__ __forceinline__ void queue_push(float4* q, int slot, const Entry& e, int pos, int idx) {
-    slot &= kQueueCap - 1;
+    if (slot >= CAP) slot -= CAP;
     q[slot * 3 + 0] = e.v0;
     q[slot * 3 + 1] = make_float4(e.v1.x, e.v1.y, e.v1.z, __int_as_float(pos));
     q[slot * 3 + 2] = make_float4(e.v2.x, e.v2.y, e.v2.z, __int_as_float(idx));
+}
+
+// Pads the queue up to a multiple of GROUP with entries no pixel can take (zero
+// opacity, threshold -inf, position past every list, splat index -1), so that the
+// last, partial group runs through the same unrolled code as the others.
+template <int CAP, int GROUP>
+__device__ __forceinline__ int queue_pad(float4* q, int head, int qn, int lane) {
+    const int pad = (GROUP - qn % GROUP) % GROUP;
+    if (lane < pad) {
+        int slot = head + qn + lane;
+        if (slot >= CAP) slot -= CAP;
+        q[slot * 3 + 0] = make_float4(0.f, 0.f, 0.f, 0.f);
+        q[slot * 3 + 1] = make_float4(0.f, 0.f, -3.0e38f, __int_as_float(0x7fffffff));
+        q[slot * 3 + 2] = make_float4(0.f, 0.f, 0.f, __int_as_float(-1));
+    }
+    return qn + pad;
 }
 
 // Where the survivor list of block `blk` (0..7, the forward's warp index) of a tile
@@ -243,8 +275,9 @@ __device__ __forceinline__ size_t survivor_list_offset(int beg, int end, int blk
 }
 
 // ------------------------------------------------------------------ forward
-constexpr int kFwdBatch = 32;
 constexpr int kGroup = 8;  // survivors composited speculatively between two guard-band checks
+constexpr int kFwdQueueCap = 40;  // 32 appended per chunk on top of at most kGroup - 1 left over
+
 
 // A pixel is live while its transmittance is at or above the floor
 // (rasterizer.cpp:100 leaves the loop the first time T < 1e-4); lanes outside
@@ -279,7 +312,7 @@ __device__ __forceinline__ void fwd_visit(const KParams& kp, const float4* __res
     fast_decide<FAM, false>(kp, m, s1.z, s1.y, hit, near, a_raw, w, dwdm);
     float alpha = fminf(kAlphaClampF, a_raw);
     if constexpr (CAREFUL) {
-        if (kp.exact && near && live) {
+        if (kp.exact && near && live && __float_as_int(s2.w) >= 0) {
             const float4 r = exact_decide(kp, recs, __float_as_int(s2.w), fx, fy);
             hit = __float_as_int(r.w) & 1;
             alpha = r.x;
@@ -304,13 +337,14 @@ __device__ __forceinline__ void fwd_visit(const KParams& kp, const float4* __res
 
 template <int FAM>
 __global__ void __launch_bounds__(kThreads, 3)
-render_fwd_kernel(KParams kp, const float4* __restrict__ recs, const int2* __restrict__ ranges,
+render_fwd_kernel(KParams kp, const float4* __restrict__ recs, const float4* __restrict__ stream,
+                  size_t stream_stride, const int2* __restrict__ ranges,
                   const int* __restrict__ point_list, int W, int H, int tiles_x, float bg0,
                   float bg1, float bg2, float* __restrict__ image, float* __restrict__ t_final,
                   int* __restrict__ processed, int* __restrict__ contributors,
-                  int2* __restrict__ surv, int* __restrict__ surv_count,
+                  float4* __restrict__ surv, size_t surv_stride, int* __restrict__ surv_count,
                   unsigned long long* __restrict__ counters) {
-    __shared__ float4 queue[kWarpsPerCta][kQueueCap * 3];
+    __shared__ float4 queue[kWarpsPerCta][kFwdQueueCap * 3];
     const int tile = blockIdx.x;
     // the warp index through a warp reduction: the compiler then knows it is warp-uniform and
     // keeps the block rectangle, queue pointer and loop control in uniform registers
@@ -336,61 +370,49 @@ render_fwd_kernel(KParams kp, const float4* __restrict__ recs, const int2* __res
     float4* q = queue[warp];
     const unsigned lt_mask = (1u << lane) - 1u;
     int head = 0, qn = 0;  // ring: entries [head, head + qn)
-    // this block's survivor list (splat index, list position), kept for the backward pass
-    int2* sl = surv + survivor_list_offset(beg, end, warp);
+    // this block's survivors, in queue format, kept for the backward pass (three arrays v0 | v1 | v2)
+    float4* sl = surv + survivor_list_offset(beg, end, warp);
 
-    // software pipeline: indices two chunks ahead, records one chunk ahead
-    int idx_cur = load_index(point_list, beg + lane, beg, end);
-    int idx_nxt = load_index(point_list, beg + 32 + lane, beg, end);
-    Entry cur, nxt;
-    load_entry(cur, recs, idx_cur);
+    // One register set holds the chunk under test and is reloaded with the next chunk as soon as
+    // its entries have been queued, so the loads fly during the compositing below.
+    Entry e;
+    int idx = -1;
+    load_entry(e, idx, stream, stream_stride, point_list, beg + lane, end);
     for (int base = beg; base < end; base += 32) {
-        load_entry(nxt, recs, idx_nxt);
-        const int idx_nn = load_index(point_list, base + 64 + lane, beg, end);
-        const bool survive =
-            idx_cur >= 0 && block_survives(cur.v0.x, cur.v0.y, cur.v0.z, cur.v0.w, cur.v1.x, cur.v1.w,
-                                           cur.v2.w, cur.v1.z, band2, X0, X1, Y0, Y1);
+        const int pos = base - beg + lane;
+        const bool survive = base + lane < end && block_survives(e.v0.x, e.v0.y, e.v0.z, e.v0.w, e.v1.x, e.v1.w,
+                                                                 e.v2.w, e.v1.z, band2, X0, X1, Y0, Y1);
         const unsigned mask = __ballot_sync(kFull, survive);
         if (survive) {
             const int rank = __popc(mask & lt_mask);
-            queue_push(q, head + qn + rank, cur, base - beg + lane, idx_cur);
-            sl[nsurv + rank] = make_int2(idx_cur, base - beg + lane);
+            queue_push<kFwdQueueCap>(q, head + qn + rank, e, pos, idx);
+            float4* dst = sl + nsurv + rank;
+            dst[0] = e.v0;
+            dst[surv_stride] = make_float4(e.v1.x, e.v1.y, e.v1.z, __int_as_float(pos));
+            dst[2 * surv_stride] = make_float4(e.v2.x, e.v2.y, e.v2.z, __int_as_float(idx));
         }
         const int cnt = __popc(mask);
         qn += cnt;
         nsurv += cnt;
-        const bool last = base + 32 >= end;
-        if (qn >= kFwdBatch || (last && qn > 0)) {
-            __syncwarp();
-            while (qn >= kFwdBatch) {
-                const float4* qb = q + head * 3;
-                for (int j0 = 0; j0 < kFwdBatch; j0 += kGroup) {
-                    const FwdPixel save = px;
-                    bool near_acc = false;
+        load_entry(e, idx, stream, stream_stride, point_list, base + 32 + lane, end);
+        if (base + 32 >= end) qn = queue_pad<kFwdQueueCap, kGroup>(q, head, qn, lane);
+        if (qn < kGroup) continue;
+        __syncwarp();
+        do {
+            const float4* qb = q + head * 3;
+            const FwdPixel save = px;
+            bool near_acc = false;
 #pragma unroll
-                    for (int j = 0; j < kGroup; ++j)
-                        fwd_visit<FAM, false>(kp, recs, qb + (j0 + j) * 3, fx, fy, px, near_acc);
-                    if (kp.exact && __any_sync(kFull, near_acc)) {  // a few groups per thousand
-                        px = save;
-                        for (int j = 0; j < kGroup; ++j)
-                            fwd_visit<FAM, true>(kp, recs, qb + (j0 + j) * 3, fx, fy, px, near_acc);
-                    }
-                }
-                head = (head + kFwdBatch) & (kQueueCap - 1);
-                qn -= kFwdBatch;
+            for (int j = 0; j < kGroup; ++j) fwd_visit<FAM, false>(kp, recs, qb + j * 3, fx, fy, px, near_acc);
+            if (kp.exact && __any_sync(kFull, near_acc)) {  // a few groups per thousand
+                px = save;
+                for (int j = 0; j < kGroup; ++j) fwd_visit<FAM, true>(kp, recs, qb + j * 3, fx, fy, px, near_acc);
             }
-            if (last) {
-                const float4* qb = q + head * 3;
-                bool unused = false;
-                for (int j = 0; j < qn; ++j) fwd_visit<FAM, true>(kp, recs, qb + j * 3, fx, fy, px, unused);
-                qn = 0;
-            }
-            __syncwarp();
-            if (!__any_sync(kFull, !(px.T < kTFloorF))) break;
-        }
-        cur = nxt;
-        idx_cur = idx_nxt;
-        idx_nxt = idx_nn;
+            head = head + kGroup == kFwdQueueCap ? 0 : head + kGroup;
+            qn -= kGroup;
+        } while (qn >= kGroup);
+        __syncwarp();
+        if (!__any_sync(kFull, !(px.T < kTFloorF))) break;
     }
     // pixels whose transmittance came within the guard band of the floor: the last value
     // (the first below the floor, or the final one) and, for a pixel that crossed, the value
@@ -447,6 +469,9 @@ constexpr int kBwdWarps = 4;
 constexpr int kBwdThreads = 32 * kBwdWarps;
 constexpr int kBwdBatch = 16;
 constexpr int kXStride = kBwdBatch + 1;  // odd: conflict-free both by row and by column
+constexpr int kBwdQueueCap = 48;         // 32 appended per chunk on top of at most kBwdBatch - 1 left over
+// per warp: queue, staging ring, 32 pixel gradients, three 32 x kXStride exchange matrices
+constexpr int kSplatGradStride = 12;     // internal gradient rows are padded to 12 floats for 128-bit atomics
 
 struct BwdPixel {
     float T;       // transmittance in front of the cursor
@@ -474,7 +499,7 @@ __device__ __forceinline__ void bwd_visit(const KParams& kp, const float4* __res
     float alpha = fminf(kAlphaClampF, a_raw);
     bool gate = a_raw < kAlphaClampF;
     if constexpr (CAREFUL) {
-        if (kp.exact && near && elig) {
+        if (kp.exact && near && elig && __float_as_int(s2.w) >= 0) {
             const float4 r = exact_decide(kp, recs, __float_as_int(s2.w), fx, fy);
             const int flags = __float_as_int(r.w);
             hit = flags & 1;
@@ -506,13 +531,14 @@ __device__ __forceinline__ void bwd_visit(const KParams& kp, const float4* __res
 }
 
 template <int FAM>
-__global__ void __launch_bounds__(kBwdThreads)
+__global__ void __launch_bounds__(kBwdThreads, 4)
 render_bwd_kernel(KParams kp, const float4* __restrict__ recs, const int2* __restrict__ ranges,
-                  const int2* __restrict__ surv, const int* __restrict__ surv_count, int W, int H,
-                  int tiles_x, float bg0, float bg1, float bg2, const float* __restrict__ grad_image,
+                  const float4* __restrict__ surv, size_t surv_stride,
+                  const int* __restrict__ surv_count, int W, int H, int tiles_x, float bg0, float bg1,
+                  float bg2, const float* __restrict__ grad_image,
                   const float* __restrict__ t_final, const int* __restrict__ processed,
                   float* __restrict__ grads, unsigned long long* __restrict__ counters) {
-    __shared__ float4 queue[kBwdWarps][kQueueCap * 3];
+    __shared__ float4 queue[kBwdWarps][kBwdQueueCap * 3];
     __shared__ float xch[kBwdWarps][3][32 * kXStride];
     __shared__ float4 gpix[kBwdWarps][32];
     const int tile = blockIdx.x >> 1, half = blockIdx.x & 1;
@@ -545,10 +571,11 @@ render_bwd_kernel(KParams kp, const float4* __restrict__ recs, const int2* __res
     px.s = (px.g0 * bg0 + px.g1 * bg1 + px.g2 * bg2) * px.T;
 
     float4* q = queue[warp];
+    float4* gp = gpix[warp];
     float* xw = xch[warp][0];
     float* xy = xch[warp][1];
     float* xz = xch[warp][2];
-    gpix[warp][lane] = make_float4(px.g0, px.g1, px.g2, 0.f);
+    gp[lane] = make_float4(px.g0, px.g1, px.g2, 0.f);
     const unsigned lt_mask = (1u << lane) - 1u;
     int head = 0, qn = 0;
 
@@ -557,59 +584,61 @@ render_bwd_kernel(KParams kp, const float4* __restrict__ recs, const int2* __res
     const float* rw = xw + (sh * 16) * kXStride + sj;
     const float* ry = xy + (sh * 16) * kXStride + sj;
     const float* rz = xz + (sh * 16) * kXStride + sj;
-    const float4* rg = gpix[warp] + sh * 16;
+    const float4* rg = gp + sh * 16;
     const float ex0 = X0, ey0 = Y0 + 2.f * sh;
 
-    // The block's survivors, as the forward queued them, walked from the back: lane l of a
-    // chunk takes the l-th entry from the chunk's end, so lane order is descending list
-    // position.  Entries the forward queued beyond the last position any of this block's
-    // pixels processed (at most a batch and a half) are dropped here.
-    const int2* sl = surv + survivor_list_offset(range.x, range.y, blk);
+    // The block's survivors, in the queue format the forward left them in, walked from the
+    // back: lane l of a chunk takes the l-th entry from the chunk's end, so lane order is
+    // descending list position and the loads are contiguous.  Entries the forward queued beyond
+    // the last position any of this block's pixels processed are dropped here.
+    const float4* sl = surv + survivor_list_offset(range.x, range.y, blk);
     const int nsl = surv_count[tile * kWarpsPerCta + blk];
-    auto load_ref = [&](int k) { return k >= 0 ? __ldg(sl + k) : make_int2(-1, 0); };
-    int2 ref_cur = load_ref(nsl - 1 - lane);
-    int2 ref_nxt = load_ref(nsl - 33 - lane);
-    Entry cur, nxt;
-    load_entry(cur, recs, ref_cur.x);
+    auto load_surv = [&](Entry& e, int k) {
+        if (k >= 0) {
+            e.v0 = __ldg(sl + k);
+            e.v1 = __ldg(sl + surv_stride + k);
+            e.v2 = __ldg(sl + 2 * surv_stride + k);
+        }
+    };
+    Entry e;
+    load_surv(e, nsl - 1 - lane);
     for (int top = nsl; top > 0; top -= 32) {
-        load_entry(nxt, recs, ref_nxt.x);
-        const int2 ref_nn = load_ref(top - 65 - lane);
-        const bool survive = ref_cur.x >= 0 && ref_cur.y < wmax;
+        const bool survive = top - 1 - lane >= 0 && __float_as_int(e.v1.w) < wmax;
         const unsigned mask = __ballot_sync(kFull, survive);
-        if (survive) queue_push(q, head + qn + __popc(mask & lt_mask), cur, ref_cur.y, ref_cur.x);
+        if (survive) {
+            int slot = head + qn + __popc(mask & lt_mask);
+            if (slot >= kBwdQueueCap) slot -= kBwdQueueCap;
+            q[slot * 3 + 0] = e.v0;
+            q[slot * 3 + 1] = e.v1;
+            q[slot * 3 + 2] = e.v2;
+        }
         qn += __popc(mask);
-        const bool last = top <= 32;
-        while (qn >= kBwdBatch || (last && qn > 0)) {
-            const int n = qn < kBwdBatch ? qn : kBwdBatch;
+        load_surv(e, top - 33 - lane);
+        if (top <= 32) qn = queue_pad<kBwdQueueCap, kBwdBatch>(q, head, qn, lane);
+        while (qn >= kBwdBatch) {
             const float4* qb = q + head * 3;
             __syncwarp();
             // ---- sweep 1: lane = pixel
             float* ww = xw + lane * kXStride;
             float* wy = xy + lane * kXStride;
             float* wz = xz + lane * kXStride;
-            bool near_acc = false;
-            if (n == kBwdBatch) {
-                for (int j0 = 0; j0 < kBwdBatch; j0 += kGroup) {
-                    const BwdPixel save = px;
-                    near_acc = false;
+            for (int j0 = 0; j0 < kBwdBatch; j0 += kGroup) {
+                const BwdPixel save = px;
+                bool near_acc = false;
 #pragma unroll
+                for (int j = 0; j < kGroup; ++j)
+                    bwd_visit<FAM, false>(kp, recs, qb + (j0 + j) * 3, fx, fy, px, ww + j0 + j, wy + j0 + j,
+                                          wz + j0 + j, near_acc);
+                if (kp.exact && __any_sync(kFull, near_acc)) {  // a few groups per thousand
+                    px = save;
                     for (int j = 0; j < kGroup; ++j)
-                        bwd_visit<FAM, false>(kp, recs, qb + (j0 + j) * 3, fx, fy, px, ww + j0 + j, wy + j0 + j,
-                                              wz + j0 + j, near_acc);
-                    if (kp.exact && __any_sync(kFull, near_acc)) {  // a few groups per thousand
-                        px = save;
-                        for (int j = 0; j < kGroup; ++j)
-                            bwd_visit<FAM, true>(kp, recs, qb + (j0 + j) * 3, fx, fy, px, ww + j0 + j, wy + j0 + j,
-                                                 wz + j0 + j, near_acc);
-                    }
+                        bwd_visit<FAM, true>(kp, recs, qb + (j0 + j) * 3, fx, fy, px, ww + j0 + j, wy + j0 + j,
+                                             wz + j0 + j, near_acc);
                 }
-            } else {
-                for (int j = 0; j < n; ++j)
-                    bwd_visit<FAM, true>(kp, recs, qb + j * 3, fx, fy, px, ww + j, wy + j, wz + j, near_acc);
             }
             __syncwarp();
             // ---- sweep 2: lane = (survivor, half of the pixels)
-            if (sj < n) {
+            {
                 const float4 r0 = qb[sj * 3 + 0];
                 const float4 r1 = qb[sj * 3 + 1];
                 const float4 r2 = qb[sj * 3 + 2];
@@ -636,42 +665,40 @@ render_bwd_kernel(KParams kp, const float4* __restrict__ recs, const int2* __res
                     sy += zy;
                 }
                 // fold the two pixel halves (lanes l and l ^ 16 hold the same survivor)
-                const unsigned pm = n >= kBwdBatch ? kFull : ((1u << n) - 1u) * 0x10001u;
-                dc0 += __shfl_xor_sync(pm, dc0, 16);
-                dc1 += __shfl_xor_sync(pm, dc1, 16);
-                dc2 += __shfl_xor_sync(pm, dc2, 16);
-                dop += __shfl_xor_sync(pm, dop, 16);
-                wsum += __shfl_xor_sync(pm, wsum, 16);
-                sxx += __shfl_xor_sync(pm, sxx, 16);
-                sxy += __shfl_xor_sync(pm, sxy, 16);
-                syy += __shfl_xor_sync(pm, syy, 16);
-                sx += __shfl_xor_sync(pm, sx, 16);
-                sy += __shfl_xor_sync(pm, sy, 16);
+                dc0 += __shfl_xor_sync(kFull, dc0, 16);
+                dc1 += __shfl_xor_sync(kFull, dc1, 16);
+                dc2 += __shfl_xor_sync(kFull, dc2, 16);
+                dop += __shfl_xor_sync(kFull, dop, 16);
+                wsum += __shfl_xor_sync(kFull, wsum, 16);
+                sxx += __shfl_xor_sync(kFull, sxx, 16);
+                sxy += __shfl_xor_sync(kFull, sxy, 16);
+                syy += __shfl_xor_sync(kFull, syy, 16);
+                sx += __shfl_xor_sync(kFull, sx, 16);
+                sy += __shfl_xor_sync(kFull, sy, 16);
                 if (sh == 0 && wsum > 0.f) {
                     // SplatGrads order d_color[3], d_opacity, d_conic_a, d_conic_b, d_conic_c, d_mu2;
                     // m = scale * (a dx^2 + 2 b dx dy + c dy^2): dm/da = scale dx^2, dm/db = 2 scale dx dy,
                     // dm/d mu = -(2A dx + B dy, B dx + 2C dy) with (A, B, C) the scaled record values.
-                    float* dst = grads + (size_t)__float_as_int(r2.w) * DARBS_GRADS_PER_SPLAT;
-                    atomicAdd(dst + 0, dc0);
-                    atomicAdd(dst + 1, dc1);
-                    atomicAdd(dst + 2, dc2);
-                    atomicAdd(dst + 3, dop);
-                    atomicAdd(dst + 4, kp.scale * sxx);
-                    atomicAdd(dst + 5, 2.f * kp.scale * sxy);
-                    atomicAdd(dst + 6, kp.scale * syy);
-                    atomicAdd(dst + 7, -fmaf(2.f * r0.z, sx, r0.w * sy));
+                    float* dst = grads + (size_t)__float_as_int(r2.w) * kSplatGradStride;
+                    atomicAdd(reinterpret_cast<float4*>(dst), make_float4(dc0, dc1, dc2, dop));
+                    atomicAdd(reinterpret_cast<float4*>(dst) + 1,
+                              make_float4(kp.scale * sxx, 2.f * kp.scale * sxy, kp.scale * syy,
+                                          -fmaf(2.f * r0.z, sx, r0.w * sy)));
                     atomicAdd(dst + 8, -fmaf(r0.w, sx, 2.f * r1.x * sy));
                 }
             }
-            head = (head + n) & (kQueueCap - 1);
-            qn -= n;
+            head = head + kBwdBatch == kBwdQueueCap ? 0 : head + kBwdBatch;
+            qn -= kBwdBatch;
         }
-        cur = nxt;
-        ref_cur = ref_nxt;
-        ref_nxt = ref_nn;
     }
     const unsigned nexact = __reduce_add_sync(kFull, px.nexact);
     if (lane == 0 && nexact) atomicAdd(counters + CNT_EXACT, (unsigned long long)nexact);
+}
+
+__global__ void export_grads_kernel(int64_t count, const float* __restrict__ padded, float* __restrict__ out) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= count) return;
+    out[i] = padded[(i / DARBS_GRADS_PER_SPLAT) * kSplatGradStride + i % DARBS_GRADS_PER_SPLAT];
 }
 
 // ------------------------------------------------------------- eval (tests)
@@ -745,24 +772,37 @@ darbs_status launch_pack(darbs_cuda_ctx* ctx, const KParams& kp, int64_t n, cons
     return check_launch(ctx, "pack_kernel");
 }
 
+// Copies the records of the K sorted list entries into list order (see load_entry).
+darbs_status launch_gather(darbs_cuda_ctx* ctx) {
+    const int64_t k = ctx->fwd_entries;
+    DARBS_TRY(reserve(ctx, ctx->stream_recs, sizeof(float4) * 3 * (size_t)(k > 0 ? k : 1)));
+    if (k == 0) return DARBS_OK;
+    gather_kernel<<<(unsigned)((k + 255) / 256), 256, 0, ctx->stream>>>(
+        k, point_list_ptr(ctx), (const float4*)ctx->recs.ptr, (float4*)ctx->stream_recs.ptr);
+    return check_launch(ctx, "gather_kernel");
+}
+
 darbs_status launch_render_fwd(darbs_cuda_ctx* ctx, const KParams& kp, int width, int height,
                                const float bg[3], float* image, float* t_final,
                                int32_t* processed, int32_t* contributors) {
     int tiles = ctx->tiles_x * ctx->tiles_y;
     if (tiles == 0) return DARBS_OK;
-    // per-block survivor lists for the backward pass: 8 regions per tile, each as long as the
+    // per-block survivor streams for the backward pass: 8 regions per tile, each as long as the
     // tile's list (address space only; the forward writes survivors, a quarter of it or less)
     const size_t k = (size_t)(ctx->fwd_entries > 0 ? ctx->fwd_entries : 1);
-    DARBS_TRY(reserve(ctx, ctx->surv, sizeof(int2) * kWarpsPerCta * k));
+    const size_t surv_stride = kWarpsPerCta * k;
+    DARBS_TRY(reserve(ctx, ctx->surv, sizeof(float4) * 3 * surv_stride));
     DARBS_TRY(reserve(ctx, ctx->surv_count, sizeof(int) * kWarpsPerCta * (size_t)tiles));
+    ctx->surv_stride = (int64_t)surv_stride;
     auto* counters = (unsigned long long*)ctx->counters.ptr;
     const float4* recs = (const float4*)ctx->recs.ptr;
     const int2* ranges = (const int2*)ctx->ranges.ptr;
     const int* plist = point_list_ptr(ctx);
-#define DARBS_LAUNCH_FWD(F)                                                                     \
-    render_fwd_kernel<F><<<tiles, kThreads, 0, ctx->stream>>>(                                  \
-        kp, recs, ranges, plist, width, height, ctx->tiles_x, bg[0], bg[1], bg[2], image,       \
-        t_final, processed, contributors, (int2*)ctx->surv.ptr, (int*)ctx->surv_count.ptr, counters)
+#define DARBS_LAUNCH_FWD(F)                                                                       \
+    render_fwd_kernel<F><<<tiles, kThreads, 0, ctx->stream>>>(                                    \
+        kp, recs, (const float4*)ctx->stream_recs.ptr, k, ranges, plist, width, height,           \
+        ctx->tiles_x, bg[0], bg[1], bg[2], image, t_final, processed, contributors,               \
+        (float4*)ctx->surv.ptr, surv_stride, (int*)ctx->surv_count.ptr, counters)
     switch (kp.fam) {
         case FAM_GAUSS2: DARBS_LAUNCH_FWD(FAM_GAUSS2); break;
         case FAM_HCOS2: DARBS_LAUNCH_FWD(FAM_HCOS2); break;
@@ -774,20 +814,24 @@ darbs_status launch_render_fwd(darbs_cuda_ctx* ctx, const KParams& kp, int width
     return check_launch(ctx, "render_fwd_kernel");
 }
 
+// Accumulates into ctx->splat_grads, n rows of kSplatGradStride floats (SplatGrads order in the
+// first nine), zeroed here.
 darbs_status launch_render_bwd(darbs_cuda_ctx* ctx, const KParams& kp, int width, int height,
                                const float bg[3], const float* grad_image, const float* t_final,
-                               const int32_t* processed, int64_t n, float* grads) {
-    DARBS_CUDA_TRY(ctx, cudaMemsetAsync(grads, 0, sizeof(float) * DARBS_GRADS_PER_SPLAT * (size_t)n,
-                                        ctx->stream));
+                               const int32_t* processed, int64_t n) {
+    const size_t bytes = sizeof(float) * kSplatGradStride * (size_t)(n > 0 ? n : 1);
+    DARBS_TRY(reserve(ctx, ctx->splat_grads, bytes));
+    DARBS_CUDA_TRY(ctx, cudaMemsetAsync(ctx->splat_grads.ptr, 0, bytes, ctx->stream));
     int tiles = ctx->tiles_x * ctx->tiles_y;
     if (tiles == 0 || n == 0) return DARBS_OK;
     auto* counters = (unsigned long long*)ctx->counters.ptr;
     const float4* recs = (const float4*)ctx->recs.ptr;
     const int2* ranges = (const int2*)ctx->ranges.ptr;
-#define DARBS_LAUNCH_BWD(F)                                                                    \
-    render_bwd_kernel<F><<<2 * tiles, kBwdThreads, 0, ctx->stream>>>(                                \
-        kp, recs, ranges, (const int2*)ctx->surv.ptr, (const int*)ctx->surv_count.ptr, width, height,   \
-        ctx->tiles_x, bg[0], bg[1], bg[2], grad_image, t_final, processed, grads, counters)
+#define DARBS_LAUNCH_BWD(F)                                                                       \
+    render_bwd_kernel<F><<<2 * tiles, kBwdThreads, 0, ctx->stream>>>(                             \
+        kp, recs, ranges, (const float4*)ctx->surv.ptr, (size_t)ctx->surv_stride,                 \
+        (const int*)ctx->surv_count.ptr, width, height, ctx->tiles_x, bg[0], bg[1], bg[2],        \
+        grad_image, t_final, processed, (float*)ctx->splat_grads.ptr, counters)
     switch (kp.fam) {
         case FAM_GAUSS2: DARBS_LAUNCH_BWD(FAM_GAUSS2); break;
         case FAM_HCOS2: DARBS_LAUNCH_BWD(FAM_HCOS2); break;
@@ -797,6 +841,15 @@ darbs_status launch_render_bwd(darbs_cuda_ctx* ctx, const KParams& kp, int width
     }
 #undef DARBS_LAUNCH_BWD
     return check_launch(ctx, "render_bwd_kernel");
+}
+
+// ctx->splat_grads (padded rows) -> out[9 n], the SplatGrads layout of the ABI.
+darbs_status launch_export_grads(darbs_cuda_ctx* ctx, int64_t n, float* out) {
+    if (n == 0) return DARBS_OK;
+    const int64_t count = n * DARBS_GRADS_PER_SPLAT;
+    export_grads_kernel<<<(unsigned)((count + 255) / 256), 256, 0, ctx->stream>>>(
+        count, (const float*)ctx->splat_grads.ptr, out);
+    return check_launch(ctx, "export_grads_kernel");
 }
 
 darbs_status launch_eval(darbs_cuda_ctx* ctx, const KParams& kp, int64_t n, const float* dm2,
