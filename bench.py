@@ -358,7 +358,7 @@ def run_ours(args):
             "iters_per_s_e2e": args.steps * world / (per_e2e[name] * 1e-3),
             "ms_per_iter": per[name] / args.steps,
             "stage_ms": st,
-            "render_fps": 1e3 / max(st["preprocess"] + st["binning"] + st["render_fwd"], 1e-9),
+            "render_fps": 1e3 / max(st["preprocess"] + st["binning"] + st["cull"] + st["render_fwd"], 1e-9),
             "work": wc,
             "render_fwd": roof(flops_fwd, mufu_fwd, st["render_fwd"]),
             "render_bwd": roof(flops_bwd, mufu_bwd, st["render_bwd"]),
@@ -401,9 +401,13 @@ def run_ours(args):
                 "preprocess": (56 + 48) * n / (st["preprocess"] * 1e-3) / 1e9 / hbm_peak,
                 "preprocess_bwd": (36 + 56 + 56) * n / (st["preprocess_bwd"] * 1e-3) / 1e9 / hbm_peak,
                 "adam": 28 * 14 * n / (st["adam"] * 1e-3) / 1e9 / hbm_peak,
-                # rect 60 B + depth sort (4 digit passes x 16 B + 4 B histogram read) + pack 108 B per
-                # splat; duplicate 8 B + tile sort (2 passes x 16 B + 4 B) + ranges 4 B per tile entry
-                "binning_sort": (236 * n + 48 * kk) / (st["binning"] * 1e-3) / 1e9 / hbm_peak,
+                # rect 60 B + depth sort (4 digit passes x 16 B + 4 B histogram read) per splat;
+                # duplicate 8 B + tile sort (2 passes x 16 B + 4 B) + ranges 4 B per tile entry
+                "binning_sort": (128 * n + 48 * kk) / (st["binning"] * 1e-3) / 1e9 / hbm_peak,
+                # pack 44 B in + 64 B out per splat; cull: 4 B index + 48 B record gather per tile entry
+                # (L2-resident records: not HBM) and 48 B written per surviving (block, entry) pair
+                "cull": (108 * n + 4 * kk + 48 * per_kernel[name]["work"]["survivors"]) / (st["cull"] * 1e-3) / 1e9
+                / hbm_peak,
             }
 
     line = {

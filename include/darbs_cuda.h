@@ -234,13 +234,14 @@ DARBS_API darbs_status darbs_cuda_adam_step(darbs_cuda_ctx* ctx, int64_t dim, fl
 
 /* Device time in milliseconds of the stages of the last forward / backward /
  * evaluate_view on this context, measured with CUDA events on the context's
- * stream (synchronises).  out[0..7] = preprocess, binning, render_fwd, loss,
- * render_bwd, preprocess_bwd, adam, reserved.  Recording is off by default. */
+ * stream (synchronises).  out[0..7] = preprocess, binning (sort and tile ranges),
+ * render_fwd, loss, render_bwd, preprocess_bwd, adam, cull (record packing and
+ * the per-block survivor streams).  Recording is off by default. */
 DARBS_API darbs_status darbs_cuda_set_stage_timing(darbs_cuda_ctx* ctx, int enabled);
 DARBS_API darbs_status darbs_cuda_stage_times(darbs_cuda_ctx* ctx, double out_ms[8]);
 /* Work counters of the last forward: out[0] = K tile entries, out[1] = sum of
- * processed (visits), out[2] = sum of contributors, out[3] = (warp, entry)
- * pairs that survived the block-level cull, out[4] = FP64 guard-band
+ * processed (visits), out[2] = sum of contributors, out[3] = (8x4 pixel block,
+ * entry) pairs that survived the block-level cull, out[4] = FP64 guard-band
  * re-decisions, out[5] = pixels flagged near the transmittance floor.
  * Synchronises. */
 DARBS_API darbs_status darbs_cuda_work_counters(darbs_cuda_ctx* ctx, int64_t out[8]);

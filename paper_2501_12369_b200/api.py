@@ -276,7 +276,7 @@ class Context:
     def stage_times(self) -> dict:
         out = (C.c_double * 8)()
         self._check(_lib.darbs_cuda_stage_times(self._h, out))
-        names = ["preprocess", "binning", "render_fwd", "loss", "render_bwd", "preprocess_bwd", "adam"]
+        names = ["preprocess", "binning", "render_fwd", "loss", "render_bwd", "preprocess_bwd", "adam", "cull"]
         return {k: float(out[i]) for i, k in enumerate(names)}
 
     def microbench(self) -> dict:

@@ -173,6 +173,32 @@ struct Stager {
         pending[npending++] = {p, b.ptr, sizeof(T) * count};
         return DARBS_OK;
     }
+    // Upload that the call consumes late: runs on the context's copy stream, behind everything
+    // already queued on the main stream (the previous call may still read the staging buffer);
+    // the caller puts await_late() in front of the first kernel that reads it.
+    template <typename T>
+    darbs_status in_late(const T* p, size_t count, const T** out) {
+        if (space == DARBS_DEVICE || p == nullptr || count == 0) {
+            *out = p;
+            return DARBS_OK;
+        }
+        if (in_slot >= 8) return fail(ctx, DARBS_CUDA_ERROR, "staging slots exhausted");
+        DeviceBuffer& b = ctx->stage_in[in_slot++];
+        DARBS_TRY(reserve(ctx, b, sizeof(T) * count));
+        DARBS_CUDA_TRY(ctx, cudaEventRecord(ctx->copy_begin, ctx->stream));
+        DARBS_CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->copy_stream, ctx->copy_begin, 0));
+        DARBS_CUDA_TRY(ctx, cudaMemcpyAsync(b.ptr, p, sizeof(T) * count, cudaMemcpyHostToDevice, ctx->copy_stream));
+        DARBS_CUDA_TRY(ctx, cudaEventRecord(ctx->copy_done, ctx->copy_stream));
+        late = true;
+        *out = (const T*)b.ptr;
+        return DARBS_OK;
+    }
+    darbs_status await_late() {
+        if (late) DARBS_CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->stream, ctx->copy_done, 0));
+        late = false;
+        return DARBS_OK;
+    }
+    bool late = false;
     // in-out host array (accumulators)
     template <typename T>
     darbs_status inout(T* p, size_t count, T** dev) {
@@ -204,7 +230,7 @@ struct DeviceGuard {
 };
 
 // ---- stage timing ------------------------------------------------------------
-enum { ST_PREPROCESS = 0, ST_BINNING, ST_RENDER_FWD, ST_LOSS, ST_RENDER_BWD, ST_PREPROCESS_BWD, ST_ADAM };
+enum { ST_PREPROCESS = 0, ST_BINNING, ST_RENDER_FWD, ST_LOSS, ST_RENDER_BWD, ST_PREPROCESS_BWD, ST_ADAM, ST_CULL };
 
 struct StageScope {
     darbs_cuda_ctx* ctx;
@@ -235,8 +261,11 @@ darbs_status forward_device(darbs_cuda_ctx* ctx, const KParams& kp, int64_t n, c
     {
         StageScope ts(ctx, ST_BINNING);
         DARBS_TRY(run_binning(ctx, n, mu2, conic, radius, depth, valid, width, height));
+    }
+    {
+        StageScope ts(ctx, ST_CULL);
         DARBS_TRY(launch_pack(ctx, kp, n, mu2, conic, opacity, rgb));
-        DARBS_TRY(launch_gather(ctx));
+        DARBS_TRY(launch_cull(ctx, kp));
     }
     DARBS_TRY(reserve(ctx, ctx->t_final, sizeof(float) * (px ? px : 1)));
     DARBS_TRY(reserve(ctx, ctx->processed, sizeof(int32_t) * (px ? px : 1)));
@@ -296,6 +325,9 @@ darbs_status darbs_cuda_create(int device, darbs_cuda_ctx** out_ctx) {
         return cuda_fail(nullptr, e, "cudaStreamCreate");
     }
     ctx->stream = ctx->own_stream;
+    cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking);
+    cudaEventCreateWithFlags(&ctx->copy_begin, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&ctx->copy_done, cudaEventDisableTiming);
     for (int i = 0; i < 16; ++i) cudaEventCreate(&ctx->timer.ev[i]);
     ctx->timer.created = true;
     darbs_status st = reserve(ctx, ctx->counters, 256);
@@ -316,7 +348,7 @@ void darbs_cuda_destroy(darbs_cuda_ctx* ctx) {
     DeviceGuard guard(ctx->device);
     cudaStreamSynchronize(ctx->stream);
     DeviceBuffer* bufs[] = {&ctx->recs, &ctx->rects, &ctx->depth_keys, &ctx->order, &ctx->offsets,
-                            &ctx->tile_keys, &ctx->tile_vals, &ctx->ranges, &ctx->stream_recs, &ctx->surv, &ctx->surv_count, &ctx->cub_temp,
+                            &ctx->tile_keys, &ctx->tile_vals, &ctx->ranges, &ctx->streams, &ctx->stream_count, &ctx->cub_temp,
                             &ctx->counters, &ctx->t_final, &ctx->processed, &ctx->contributors,
                             &ctx->image, &ctx->valid, &ctx->splat_grads, &ctx->grad_image};
     for (DeviceBuffer* b : bufs)
@@ -328,6 +360,9 @@ void darbs_cuda_destroy(darbs_cuda_ctx* ctx) {
     if (ctx->pinned) cudaFreeHost(ctx->pinned);
     if (ctx->timer.created)
         for (int i = 0; i < 16; ++i) cudaEventDestroy(ctx->timer.ev[i]);
+    if (ctx->copy_begin) cudaEventDestroy(ctx->copy_begin);
+    if (ctx->copy_done) cudaEventDestroy(ctx->copy_done);
+    if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
     if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
     delete ctx;
 }
@@ -467,7 +502,7 @@ darbs_status darbs_cuda_forward(darbs_cuda_ctx* ctx, const darbs_kernel_spec* ke
     DeviceGuard guard(ctx->device);
     KParams kp;
     DARBS_TRY(make_kparams(ctx, kernel, &kp));
-    reset_stage_marks(ctx, {ST_BINNING, ST_RENDER_FWD});
+    reset_stage_marks(ctx, {ST_BINNING, ST_CULL, ST_RENDER_FWD});
     Stager st(ctx, space);
     const float *d_mu2, *d_conic, *d_radius, *d_depth, *d_opacity, *d_rgb;
     DARBS_TRY(st.in(mu2, 2 * (size_t)n, &d_mu2));
@@ -656,7 +691,7 @@ darbs_status darbs_cuda_evaluate_view(darbs_cuda_ctx* ctx, const darbs_kernel_sp
     const int width = cam.width, height = cam.height;
     if (width <= 0 || height <= 0) return fail(ctx, DARBS_INVALID_PARAMETER, "camera has no pixels");
     const size_t px = (size_t)width * height, nn = (size_t)n;
-    reset_stage_marks(ctx, {ST_PREPROCESS, ST_BINNING, ST_RENDER_FWD, ST_LOSS, ST_RENDER_BWD, ST_PREPROCESS_BWD});
+    reset_stage_marks(ctx, {ST_PREPROCESS, ST_BINNING, ST_CULL, ST_RENDER_FWD, ST_LOSS, ST_RENDER_BWD, ST_PREPROCESS_BWD});
 
     Stager st(ctx, param_space);
     Stager sti(ctx, image_space);
@@ -665,7 +700,7 @@ darbs_status darbs_cuda_evaluate_view(darbs_cuda_ctx* ctx, const darbs_kernel_sp
     const float *d_raw, *d_target, *d_gimg;
     float *d_pgrads, *d_image;
     DARBS_TRY(st.in(raw_params, 14 * nn, &d_raw));
-    DARBS_TRY(sti.in(target, 3 * px, &d_target));
+    DARBS_TRY(sti.in_late(target, 3 * px, &d_target));  // not needed before the loss: overlaps the forward
     DARBS_TRY(sti.in(grad_image, 3 * px, &d_gimg));
     DARBS_TRY(st.inout(param_grads, 14 * nn, &d_pgrads));
     DARBS_TRY(sti.out(image_out, 3 * px, &d_image));
@@ -694,6 +729,7 @@ darbs_status darbs_cuda_evaluate_view(darbs_cuda_ctx* ctx, const darbs_kernel_sp
     }
     DARBS_TRY(forward_device(ctx, kp, n, d_mu2, d_conic, d_radius, d_depth, d_opacity, d_rgb, d_valid,
                              width, height, background, d_image, nullptr));
+    DARBS_TRY(sti.await_late());
     if (target) {
         StageScope ts(ctx, ST_LOSS);
         DARBS_TRY(reserve(ctx, ctx->grad_image, sizeof(float) * 3 * px));

@@ -66,6 +66,10 @@ struct darbs_cuda_ctx {
     int device = 0;
     cudaStream_t own_stream = nullptr;
     cudaStream_t stream = nullptr;
+    // host -> device uploads that a call does not need until late (the target image of
+    // evaluate_view) run on their own stream, fenced by these two events
+    cudaStream_t copy_stream = nullptr;
+    cudaEvent_t copy_begin = nullptr, copy_done = nullptr;
     std::string last_error;
     int64_t launches = 0;
     int exact = 1;
@@ -81,10 +85,8 @@ struct darbs_cuda_ctx {
     darbs_b200::DeviceBuffer tile_keys;    // 2 * K u32
     darbs_b200::DeviceBuffer tile_vals;    // 2 * K u32
     darbs_b200::DeviceBuffer ranges;       // tiles * int2
-    darbs_b200::DeviceBuffer stream_recs;  // 3 * K float4: records in list order (v0 | v1 | v2)
-    darbs_b200::DeviceBuffer surv;         // 3 * 8K float4: per-block survivor streams (v0 | v1 | v2)
-    darbs_b200::DeviceBuffer surv_count;   // 8 * tiles int
-    int64_t surv_stride = 0;               // 8K, the length of one of the three survivor arrays
+    darbs_b200::DeviceBuffer streams;      // 8 (K + 32 tiles) x 48 B: per-block survivor streams (render.cu)
+    darbs_b200::DeviceBuffer stream_count; // 2 x 8 tiles int: entries per stream | entries the forward composited
     darbs_b200::DeviceBuffer cub_temp;
     darbs_b200::DeviceBuffer counters;     // Counters + scalars
     darbs_b200::DeviceBuffer t_final, processed, contributors, image;  // per-pixel aux
@@ -142,7 +144,7 @@ darbs_status launch_pack(darbs_cuda_ctx* ctx, const KParams& kp, int64_t n, cons
 darbs_status launch_render_fwd(darbs_cuda_ctx* ctx, const KParams& kp, int width, int height,
                                const float bg[3], float* image, float* t_final,
                                int32_t* processed, int32_t* contributors);
-darbs_status launch_gather(darbs_cuda_ctx* ctx);
+darbs_status launch_cull(darbs_cuda_ctx* ctx, const KParams& kp);
 darbs_status launch_render_bwd(darbs_cuda_ctx* ctx, const KParams& kp, int width, int height,
                                const float bg[3], const float* grad_image, const float* t_final,
                                const int32_t* processed, int64_t n);

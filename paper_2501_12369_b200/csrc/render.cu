@@ -1,38 +1,46 @@
-// render.cu — per-tile front-to-back compositing (forward) and its reverse
-// traversal (backward) for the DARBF families, hand-written for sm_100a.
+// render.cu — block culling, per-tile front-to-back compositing (forward) and its
+// reverse traversal (backward) for the DARBF families, hand-written for sm_100a.
 //
 // Reference semantics: darbs::forward  src/rasterizer.cpp:55-112 (inner loop :85-107)
 //                      darbs::backward src/rasterizer.cpp:147-234 (inner loop :175-214)
 //
-// Design: one CTA of 8 warps per 16x16 tile (the reference's
-// kTileSize, so bins are comparable entry for entry); each warp owns an 8x4
-// pixel block and walks the tile's depth-sorted list on its own, 32 entries at
-// a time.  A lane first tests ONE entry against the warp's pixel block (exact
-// minimum of the conic's quadratic form over the block against the splat's
-// decision threshold); survivors are compacted through a per-warp shared-memory
-// stage and only those are evaluated per pixel.  No CTA-wide barrier, no
-// cross-warp dependency, so a warp whose 32 pixels have saturated leaves
-// immediately.  Entries culled at block level are still COUNTED (processed[] is
-// positional), so per-pixel aux is identical to the reference's.
+// Design.  A 16x16 tile (the reference's kTileSize, so bins are
+// comparable entry for entry) is split into eight 8x4 pixel blocks, one warp each.
 //
-// Threshold decisions (alpha >= 1/255, dm2 vs cutoff, dm2 < 0) are taken in
-// FP32 against a per-splat precomputed boundary; when the FP32 value lies
-// inside a guard band of that boundary the decision is re-taken in FP64 with
-// the reference's own expression order, so integer outputs match the FP64
-// reference.
-#include <cooperative_groups.h>
-
+//   cull_kernel   one CTA per tile walks the tile's depth-sorted list once and tests
+//                 every entry against the eight blocks (exact minimum of the conic's
+//                 quadratic form over the block against the splat's decision
+//                 threshold).  Survivors are written, in list order, to one compact
+//                 stream per block as ready-to-composite 48-byte entries
+//                 { mu.x, mu.y, A, B } { C, opacity, thr_m, list position }
+//                 { r, g, b, splat index }.
+//   render_fwd    a warp streams its block's entries into shared memory with 1-D
+//                 bulk async copies (cp.async.bulk + mbarrier: UBLKCP in SASS), three
+//                 chunks of 32 entries deep, and composites them front to back in
+//                 branch-free groups of eight.  No CTA-wide barrier: a warp whose 32
+//                 pixels have saturated leaves immediately.
+//   render_bwd    the same stream walked from the back, two sweeps per batch of 16
+//                 entries (see below), 128-bit atomics into the per-splat gradients.
+//
+// Entries culled at block level are still COUNTED (processed[] is positional), so the
+// per-pixel aux is identical to the reference's.
+//
+// Threshold decisions (alpha >= 1/255, dm2 vs cutoff, dm2 < 0) are taken in FP32
+// against a per-splat precomputed boundary; when the FP32 value lies inside a guard
+// band of that boundary the decision is re-taken in FP64 with the reference's own
+// expression order, so integer outputs match the FP64 reference.
 #include "family.cuh"
 
 namespace darbs_b200 {
 
 namespace {
 
+constexpr int kBlocksPerTile = 8;  // 2 x 4 blocks of 8 x 4 pixels
 constexpr int kWarpsPerCta = 8;
 constexpr int kThreads = 32 * kWarpsPerCta;
 constexpr unsigned kFull = 0xffffffffu;
 
-// counters (u64 each): 3 = surviving (warp, entry) pairs, 4 = FP64 re-decisions,
+// counters (u64 each): 3 = surviving (block, entry) pairs, 4 = FP64 re-decisions,
 // 5 = pixels whose transmittance came within the guard band of the floor.
 enum { CNT_SURVIVORS = 3, CNT_EXACT = 4, CNT_TFLOOR = 5 };
 
@@ -59,45 +67,7 @@ __global__ void pack_kernel(KParams kp, int64_t n, const float* __restrict__ mu2
     r[3] = make_float4(a, b, c, 0.f);
 }
 
-__global__ void gather_kernel(int64_t k, const int* __restrict__ point_list,
-                              const float4* __restrict__ recs, float4* __restrict__ stream) {
-    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (i >= k) return;
-    const float4* r = recs + kRecVecs * (int64_t)__ldg(point_list + i);
-    const float4 v0 = __ldg(r), v1 = __ldg(r + 1), v2 = __ldg(r + 2);
-    stream[i] = v0;
-    stream[k + i] = v1;
-    stream[2 * k + i] = v2;
-}
-
 // ------------------------------------------------------------ shared pieces
-
-// Lower bound of m(d) = A dx^2 + B dx dy + C dy^2 over the rectangle of pixel
-// centres [X0,X1]x[Y0,Y1] (d measured from the splat centre), for A, C > 0 and
-// 4AC > B^2 (the pack kernel sends every other conic down the NaN path).  The
-// minimum of a convex quadratic over a box that does not contain the
-// unconstrained minimiser lies on an edge facing it; evaluated branch-free:
-// candidate 1 = best point of the vertical line through the x-clamped centre,
-// candidate 2 = same for the horizontal line; when the centre is inside the
-// box both are 0, when it is outside along one axis only the candidate of the
-// other axis lies on the facing edge too and is not smaller.
-// kx = -B/(2C), ky = -B/(2A) come precomputed with the record.
-__device__ __forceinline__ bool block_survives(float mx, float my, float A, float B, float C,
-                                               float kx, float ky, float thr, float band2,
-                                               float X0, float X1, float Y0, float Y1) {
-    const float ex0 = X0 - mx, ex1 = X1 - mx, ey0 = Y0 - my, ey1 = Y1 - my;
-    const float dxc = fminf(fmaxf(0.f, ex0), ex1);
-    const float dyc = fminf(fmaxf(0.f, ey0), ey1);
-    const float dy1 = fminf(fmaxf(kx * dxc, ey0), ey1);
-    const float m1 = fmaf(fmaf(A, dxc, B * dy1), dxc, (C * dy1) * dy1);
-    const float dx2 = fminf(fmaxf(ky * dyc, ex0), ex1);
-    const float m2 = fmaf(fmaf(A, dx2, B * dyc), dx2, (C * dyc) * dyc);
-    const float mmin = fminf(m1, m2);
-    // Per-pixel decisions can only be positive for m <= thr + band; keep a
-    // relative margin for the FP32 rounding of mmin itself.  A NaN threshold
-    // (decided in FP64) compares false and survives.
-    return !(mmin * 0.9999f > thr + band2);
-}
 
 // FP32 generic evaluation of eval() for FAM_GENERIC (kernel.cpp:127-164).
 __device__ __forceinline__ void generic_eval(const KParams& kp, float dm2, float& w, float& dw) {
@@ -214,70 +184,215 @@ __device__ __forceinline__ float quad_m(float A, float B, float C, float dx, flo
     return fmaf(fmaf(A, dx, B * dy), dx, (C * dy) * dy);
 }
 
-// One list entry as a lane holds it while testing it against the warp's block.
-struct Entry {
-    float4 v0, v1, v2;
-};
 
-// ---- tile-ordered record streams
-// After the sort, gather_kernel copies the three hot vectors of every list
-// entry's record into three arrays in LIST order (v0 | v1 | v2, each K float4),
-// so that the 8 warps of a tile read their entries with fully coalesced loads
-// (4 L1 wavefronts per load instead of one per lane for a gather through the
-// point list) and without a dependent index load.
-__device__ __forceinline__ void load_entry(Entry& e, int& idx, const float4* __restrict__ stream,
-                                           size_t stride, const int* __restrict__ point_list, int k,
-                                           int end) {
-    if (k < end) {
-        e.v0 = __ldg(stream + k);
-        e.v1 = __ldg(stream + stride + k);
-        e.v2 = __ldg(stream + 2 * stride + k);
-        idx = __ldg(point_list + k);
+// ------------------------------------------------------------ survivor streams
+// One stream entry = three float4 (48 B).  A chunk = 32 entries = 1536 B, the unit
+// of the bulk copies.  Streams are padded with null entries (zero opacity, threshold
+// -inf, position past every list, splat index -1: nothing can take them) up to a
+// whole chunk, so the compositing loops never see a partial group.
+constexpr int kEntryVecs = 3;
+constexpr int kChunk = 32;
+constexpr int kChunkVecs = kChunk * kEntryVecs;
+constexpr int kChunkBytes = kChunkVecs * (int)sizeof(float4);
+constexpr int kStages = 3;
+
+// Entry offset of block `blk`'s stream for tile `tile` whose point list is [beg, end):
+// every block owns a region as long as the tile's list rounded up to a chunk (the
+// worst case).  8 (K + 32 tiles) entries of address space; only survivors and their
+// padding are ever written or read.
+__host__ __device__ __forceinline__ size_t stream_offset(int tile, int beg, int end, int blk) {
+    const size_t cap = (size_t)((end - beg + kChunk - 1) & ~(kChunk - 1));
+    return (size_t)kBlocksPerTile * ((size_t)beg + (size_t)kChunk * (size_t)tile) + (size_t)blk * cap;
+}
+
+__device__ __forceinline__ void store_null_entry(float4* e) {
+    e[0] = make_float4(0.f, 0.f, 0.f, 0.f);
+    e[1] = make_float4(0.f, 0.f, -3.0e38f, __int_as_float(0x7fffffff));
+    e[2] = make_float4(0.f, 0.f, 0.f, __int_as_float(-1));
+}
+
+// ------------------------------------------------------------------ culling
+// Lower bound of m(d) = A dx^2 + B dx dy + C dy^2 over the rectangle of pixel
+// centres [X0,X1]x[Y0,Y1] (d measured from the splat centre), for A, C > 0 and
+// 4AC > B^2 (the pack kernel sends every other conic down the NaN path).  The
+// minimum of a convex quadratic over a box that does not contain the unconstrained
+// minimiser lies on an edge facing it; evaluated branch-free: candidate 1 = best
+// point of the vertical line through the x-clamped centre, candidate 2 = same for
+// the horizontal line; when the centre is inside the box both are 0, when it is
+// outside along one axis only the candidate of the other axis lies on the facing
+// edge too and is not smaller.  (dxc, ex0, ex1) / (dyc, ey0, ey1): clamped centre
+// and box edges per axis, shared between the blocks of a row / column.
+__device__ __forceinline__ bool block_survives(float A, float B, float C, float kx, float ky,
+                                               float thr2, float dxc, float ex0, float ex1,
+                                               float dyc, float ey0, float ey1) {
+    const float dy1 = fminf(fmaxf(kx * dxc, ey0), ey1);
+    const float m1 = fmaf(fmaf(A, dxc, B * dy1), dxc, (C * dy1) * dy1);
+    const float dx2 = fminf(fmaxf(ky * dyc, ex0), ex1);
+    const float m2 = fmaf(fmaf(A, dx2, B * dyc), dx2, (C * dyc) * dyc);
+    // Per-pixel decisions can only be positive for m <= thr + band; keep a relative
+    // margin for the FP32 rounding of the bound itself.  A NaN threshold (decided in
+    // FP64) compares false and survives.
+    return !(fminf(m1, m2) * 0.9999f > thr2);
+}
+
+// One CTA per tile; thread t of a 256-entry step takes list entry base + t, gathers its
+// record and tests it against the eight blocks.  Per block, a ballot per warp and a
+// prefix over the eight warps give every survivor its slot, so streams keep list order.
+__global__ void __launch_bounds__(kThreads)
+cull_kernel(KParams kp, const float4* __restrict__ recs, const int2* __restrict__ ranges,
+            const int* __restrict__ point_list, int tiles_x, float4* __restrict__ streams,
+            int* __restrict__ stream_count, unsigned long long* __restrict__ counters) {
+    __shared__ int wcnt[kWarpsPerCta][kBlocksPerTile];
+    __shared__ int wpre[kWarpsPerCta][kBlocksPerTile];
+    const int tile = blockIdx.x;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int2 range = ranges[tile];
+    const int beg = range.x, end = range.y;
+    const float tx0 = (float)((tile % tiles_x) * DARBS_TILE_SIZE) + 0.5f;
+    const float ty0 = (float)((tile / tiles_x) * DARBS_TILE_SIZE) + 0.5f;
+    const float band2 = 2.f * kp.band;
+    const unsigned lt_mask = (1u << lane) - 1u;
+    // threads 0..63 keep the running stream length of block (tid & 7); the eight copies agree
+    int run = 0;
+    float4* const tile_streams = streams + kEntryVecs * stream_offset(tile, beg, end, 0);
+    const size_t cap = (size_t)((end - beg + kChunk - 1) & ~(kChunk - 1));
+
+    // software pipeline: list index two steps ahead, record one step ahead of the step under test
+    int idx_n = beg + tid < end ? __ldg(point_list + beg + tid) : -1;
+    float4 n0 = make_float4(0.f, 0.f, 0.f, 0.f), n1 = n0, n2 = n0;
+    if (idx_n >= 0) {
+        const float4* r = recs + kRecVecs * (int64_t)idx_n;
+        n0 = __ldg(r);
+        n1 = __ldg(r + 1);
+        n2 = __ldg(r + 2);
+    }
+    int idx_nn = beg + kThreads + tid < end ? __ldg(point_list + beg + kThreads + tid) : -1;
+    for (int base = beg; base < end; base += kThreads) {
+        const int k = base + tid;
+        const bool valid = k < end;
+        const float4 v0 = n0, v1 = n1, v2 = n2;
+        const int idx = idx_n;
+        idx_n = idx_nn;
+        if (idx_n >= 0) {
+            const float4* r = recs + kRecVecs * (int64_t)idx_n;
+            n0 = __ldg(r);
+            n1 = __ldg(r + 1);
+            n2 = __ldg(r + 2);
+        }
+        idx_nn = k + 2 * kThreads < end ? __ldg(point_list + k + 2 * kThreads) : -1;
+        unsigned bits = 0;
+        if (valid) {
+            const float thr2 = v1.z + band2;
+            float dxc[2], ex0[2], ex1[2];
+#pragma unroll
+            for (int xb = 0; xb < 2; ++xb) {
+                ex0[xb] = tx0 + 8.f * xb - v0.x;
+                ex1[xb] = ex0[xb] + 7.f;
+                dxc[xb] = fminf(fmaxf(0.f, ex0[xb]), ex1[xb]);
+            }
+#pragma unroll
+            for (int yb = 0; yb < 4; ++yb) {
+                const float ey0 = ty0 + 4.f * yb - v0.y, ey1 = ey0 + 3.f;
+                const float dyc = fminf(fmaxf(0.f, ey0), ey1);
+#pragma unroll
+                for (int xb = 0; xb < 2; ++xb)
+                    if (block_survives(v0.z, v0.w, v1.x, v1.w, v2.w, thr2, dxc[xb], ex0[xb], ex1[xb], dyc, ey0,
+                                       ey1))
+                        bits |= 1u << (yb * 2 + xb);
+            }
+        }
+        unsigned masks[kBlocksPerTile];
+#pragma unroll
+        for (int b = 0; b < kBlocksPerTile; ++b) masks[b] = __ballot_sync(kFull, (bits >> b) & 1u);
+        if (lane < kBlocksPerTile) {
+            unsigned m = masks[0];
+#pragma unroll
+            for (int b = 1; b < kBlocksPerTile; ++b) m = lane == b ? masks[b] : m;
+            wcnt[warp][lane] = __popc(m);
+        }
+        __syncthreads();
+        if (tid < kWarpsPerCta * kBlocksPerTile) {
+            const int w = tid >> 3, b = tid & 7;
+            int pre = run, total = 0;
+#pragma unroll
+            for (int ww = 0; ww < kWarpsPerCta; ++ww) {
+                const int c = wcnt[ww][b];
+                pre += ww < w ? c : 0;
+                total += c;
+            }
+            wpre[w][b] = pre;
+            run += total;
+        }
+        __syncthreads();
+        if (bits) {
+            const float4 e1 = make_float4(v1.x, v1.y, v1.z, __int_as_float(k - beg));
+            const float4 e2 = make_float4(v2.x, v2.y, v2.z, __int_as_float(idx));
+#pragma unroll
+            for (int b = 0; b < kBlocksPerTile; ++b)
+                if ((bits >> b) & 1u) {
+                    const size_t slot = (size_t)b * cap + (size_t)(wpre[warp][b] + __popc(masks[b] & lt_mask));
+                    float4* e = tile_streams + kEntryVecs * slot;
+                    e[0] = v0;
+                    e[1] = e1;
+                    e[2] = e2;
+                }
+        }
+        // wcnt / wpre are rewritten only after the next step's first barrier / by the threads
+        // that passed this step's second barrier, so no third barrier is needed
+    }
+    // stream lengths, and null padding up to a whole chunk
+    __shared__ int total[kBlocksPerTile];
+    if (tid < kBlocksPerTile) {
+        total[tid] = run;
+        stream_count[tile * kBlocksPerTile + tid] = run;
+        atomicAdd(counters + CNT_SURVIVORS, (unsigned long long)run);
+    }
+    __syncthreads();
+    {
+        const int b = warp, n = total[b];
+        const int padded = (n + kChunk - 1) & ~(kChunk - 1);
+        if (n + lane < padded) store_null_entry(tile_streams + kEntryVecs * ((size_t)b * cap + (size_t)(n + lane)));
     }
 }
 
-// Per-warp survivor queue in shared memory: a ring of CAP entries of three
-// float4 { mu.x, mu.y, A, B } { C, opacity, thr_m, list position } { r, g, b,
-// splat index }.  Entries that pass the block test are appended in list order;
-// the compositing loops consume them in fixed-size groups that never wrap (CAP
-// is a multiple of the group size): one chunk is appended between two drains,
-// on top of less than one group left over.
-template <int CAP>
-__device__ __forceinline__ void queue_push(float4* q, int slot, const Entry& e, int pos, int idx) {
-    if (slot >= CAP) slot -= CAP;
-    q[slot * 3 + 0] = e.v0;
-    q[slot * 3 + 1] = make_float4(e.v1.x, e.v1.y, e.v1.z, __int_as_float(pos));
-    q[slot * 3 + 2] = make_float4(e.v2.x, e.v2.y, e.v2.z, __int_as_float(idx));
-}
+// ---------------------------------------------------- bulk async copies (TMA)
+__device__ __forceinline__ unsigned smem_addr(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
 
-// Pads the queue up to a multiple of GROUP with entries no pixel can take (zero
-// opacity, threshold -inf, position past every list, splat index -1), so that the
-// last, partial group runs through the same unrolled code as the others.
-template <int CAP, int GROUP>
-__device__ __forceinline__ int queue_pad(float4* q, int head, int qn, int lane) {
-    const int pad = (GROUP - qn % GROUP) % GROUP;
-    if (lane < pad) {
-        int slot = head + qn + lane;
-        if (slot >= CAP) slot -= CAP;
-        q[slot * 3 + 0] = make_float4(0.f, 0.f, 0.f, 0.f);
-        q[slot * 3 + 1] = make_float4(0.f, 0.f, -3.0e38f, __int_as_float(0x7fffffff));
-        q[slot * 3 + 2] = make_float4(0.f, 0.f, 0.f, __int_as_float(-1));
-    }
-    return qn + pad;
+__device__ __forceinline__ void mbar_init(unsigned long long* bar) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(bar)) : "memory");
 }
-
-// Where the survivor list of block `blk` (0..7, the forward's warp index) of a tile
-// whose point list is [beg, end) starts: every block owns a region as long as the
-// tile's list, the worst case.  8 * K entries of address space; only survivors are
-// ever written or read.
-__device__ __forceinline__ size_t survivor_list_offset(int beg, int end, int blk) {
-    return (size_t)beg * kWarpsPerCta + (size_t)blk * (size_t)(end - beg);
+__device__ __forceinline__ void mbar_init_fence() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+// One lane arms the barrier with the byte count and issues the copy, which arrives on it.
+__device__ __forceinline__ void bulk_load(float4* dst, const float4* src, unsigned bytes,
+                                          unsigned long long* bar) {
+    const unsigned b = smem_addr(bar);
+    // earlier generic-proxy reads of dst (previous use of the stage) are ordered before the
+    // async-proxy write by the __syncwarp that precedes this call plus this proxy fence
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(bytes) : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_addr(dst)),
+                 "l"(src), "r"(bytes), "r"(b)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_LOOP:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@p bra WAIT_DONE;\n"
+        "bra WAIT_LOOP;\n"
+        "WAIT_DONE:\n"
+        "}\n" ::"r"(smem_addr(bar)),
+        "r"(parity)
+        : "memory");
 }
 
 // ------------------------------------------------------------------ forward
-constexpr int kGroup = 8;  // survivors composited speculatively between two guard-band checks
-constexpr int kFwdQueueCap = 40;  // 32 appended per chunk on top of at most kGroup - 1 left over
-
+constexpr int kGroup = 8;  // entries composited speculatively between two guard-band checks
 
 // A pixel is live while its transmittance is at or above the floor
 // (rasterizer.cpp:100 leaves the loop the first time T < 1e-4); lanes outside
@@ -336,18 +451,18 @@ __device__ __forceinline__ void fwd_visit(const KParams& kp, const float4* __res
 }
 
 template <int FAM>
-__global__ void __launch_bounds__(kThreads, 3)
-render_fwd_kernel(KParams kp, const float4* __restrict__ recs, const float4* __restrict__ stream,
-                  size_t stream_stride, const int2* __restrict__ ranges,
-                  const int* __restrict__ point_list, int W, int H, int tiles_x, float bg0,
-                  float bg1, float bg2, float* __restrict__ image, float* __restrict__ t_final,
-                  int* __restrict__ processed, int* __restrict__ contributors,
-                  float4* __restrict__ surv, size_t surv_stride, int* __restrict__ surv_count,
+__global__ void __launch_bounds__(kThreads, 4)
+render_fwd_kernel(KParams kp, const float4* __restrict__ recs, const int2* __restrict__ ranges,
+                  const int* __restrict__ point_list, const float4* __restrict__ streams,
+                  const int* __restrict__ stream_count, int* __restrict__ stream_used, int W, int H,
+                  int tiles_x, float bg0, float bg1, float bg2, float* __restrict__ image,
+                  float* __restrict__ t_final, int* __restrict__ processed, int* __restrict__ contributors,
                   unsigned long long* __restrict__ counters) {
-    __shared__ float4 queue[kWarpsPerCta][kFwdQueueCap * 3];
+    __shared__ __align__(128) float4 ring[kWarpsPerCta][kStages][kChunkVecs];
+    __shared__ unsigned long long bars[kWarpsPerCta][kStages];
     const int tile = blockIdx.x;
     // the warp index through a warp reduction: the compiler then knows it is warp-uniform and
-    // keeps the block rectangle, queue pointer and loop control in uniform registers
+    // keeps the ring pointers and loop control in uniform registers
     const int warp = __reduce_min_sync(kFull, (int)(threadIdx.x >> 5)), lane = threadIdx.x & 31;
     const int bx = (tile % tiles_x) * DARBS_TILE_SIZE + (warp & 1) * 8;
     const int by = (tile / tiles_x) * DARBS_TILE_SIZE + (warp >> 1) * 4;
@@ -355,10 +470,8 @@ render_fwd_kernel(KParams kp, const float4* __restrict__ recs, const float4* __r
     const int pxl = bx + (lane & 7), pyl = by + (lane >> 3);
     const bool inside = pxl < W && pyl < H;
     const float fx = pxl + 0.5f, fy = pyl + 0.5f;
-    const float X0 = bx + 0.5f, X1 = bx + 7.5f, Y0 = by + 0.5f, Y1 = by + 3.5f;
     const int2 range = ranges[tile];
     const int beg = range.x, end = range.y;
-    const float band2 = 2.f * kp.band;
 
     FwdPixel px;
     px.T = inside ? 1.f : 0.f;
@@ -366,40 +479,34 @@ render_fwd_kernel(KParams kp, const float4* __restrict__ recs, const float4* __r
     px.contrib = 0.f;
     px.proc = end - beg;
     px.nexact = 0;
-    int nsurv = 0;
-    float4* q = queue[warp];
-    const unsigned lt_mask = (1u << lane) - 1u;
-    int head = 0, qn = 0;  // ring: entries [head, head + qn)
-    // this block's survivors, in queue format, kept for the backward pass (three arrays v0 | v1 | v2)
-    float4* sl = surv + survivor_list_offset(beg, end, warp);
 
-    // One register set holds the chunk under test and is reloaded with the next chunk as soon as
-    // its entries have been queued, so the loads fly during the compositing below.
-    Entry e;
-    int idx = -1;
-    load_entry(e, idx, stream, stream_stride, point_list, beg + lane, end);
-    for (int base = beg; base < end; base += 32) {
-        const int pos = base - beg + lane;
-        const bool survive = base + lane < end && block_survives(e.v0.x, e.v0.y, e.v0.z, e.v0.w, e.v1.x, e.v1.w,
-                                                                 e.v2.w, e.v1.z, band2, X0, X1, Y0, Y1);
-        const unsigned mask = __ballot_sync(kFull, survive);
-        if (survive) {
-            const int rank = __popc(mask & lt_mask);
-            queue_push<kFwdQueueCap>(q, head + qn + rank, e, pos, idx);
-            float4* dst = sl + nsurv + rank;
-            dst[0] = e.v0;
-            dst[surv_stride] = make_float4(e.v1.x, e.v1.y, e.v1.z, __int_as_float(pos));
-            dst[2 * surv_stride] = make_float4(e.v2.x, e.v2.y, e.v2.z, __int_as_float(idx));
+    const float4* src = streams + kEntryVecs * stream_offset(tile, beg, end, warp);
+    const int n = stream_count[tile * kBlocksPerTile + warp];
+    const int nchunks = (n + kChunk - 1) / kChunk;
+    float4* stage0 = ring[warp][0];
+    unsigned long long* bar = bars[warp];
+    if (lane == 0) {
+        for (int s = 0; s < kStages; ++s) mbar_init(bar + s);
+        mbar_init_fence();
+        // chunks 0 and 1 in flight before the loop; chunk c + 2 is issued while c is composited
+        if (nchunks > 0) bulk_load(stage0, src, kChunkBytes, bar);
+        if (nchunks > 1) bulk_load(stage0 + kChunkVecs, src + kChunkVecs, kChunkBytes, bar + 1);
+    }
+    __syncwarp();
+    int used = 0, stage = 0;
+    unsigned parity = 0;
+    int c = 0;
+    for (; c < nchunks; ++c) {
+        if (lane == 0 && c + 2 < nchunks) {
+            const int fill = stage == 0 ? 2 : stage - 1;  // the stage chunk c - 1 vacated
+            bulk_load(stage0 + fill * kChunkVecs, src + (size_t)(c + 2) * kChunkVecs, kChunkBytes, bar + fill);
         }
-        const int cnt = __popc(mask);
-        qn += cnt;
-        nsurv += cnt;
-        load_entry(e, idx, stream, stream_stride, point_list, base + 32 + lane, end);
-        if (base + 32 >= end) qn = queue_pad<kFwdQueueCap, kGroup>(q, head, qn, lane);
-        if (qn < kGroup) continue;
-        __syncwarp();
-        do {
-            const float4* qb = q + head * 3;
+        mbar_wait(bar + stage, parity);
+        const float4* qc = stage0 + stage * kChunkVecs;
+        const int rem = n - c * kChunk;
+        const int ngroups = rem >= kChunk ? kChunk / kGroup : (rem + kGroup - 1) / kGroup;
+        for (int g = 0; g < ngroups; ++g) {
+            const float4* qb = qc + g * (kGroup * kEntryVecs);
             const FwdPixel save = px;
             bool near_acc = false;
 #pragma unroll
@@ -408,11 +515,29 @@ render_fwd_kernel(KParams kp, const float4* __restrict__ recs, const float4* __r
                 px = save;
                 for (int j = 0; j < kGroup; ++j) fwd_visit<FAM, true>(kp, recs, qb + j * 3, fx, fy, px, near_acc);
             }
-            head = head + kGroup == kFwdQueueCap ? 0 : head + kGroup;
-            qn -= kGroup;
-        } while (qn >= kGroup);
+        }
+        used += ngroups * kGroup;
         __syncwarp();
-        if (!__any_sync(kFull, !(px.T < kTFloorF))) break;
+        if (stage == kStages - 1) {
+            stage = 0;
+            parity ^= 1u;
+        } else {
+            ++stage;
+        }
+        if (!__any_sync(kFull, !(px.T < kTFloorF))) {
+            ++c;
+            break;
+        }
+    }
+    // copies still in flight must land before the CTA's shared memory can be given away
+    for (int d = c; d < nchunks && d < c + 2; ++d) {
+        mbar_wait(bar + stage, parity);
+        if (stage == kStages - 1) {
+            stage = 0;
+            parity ^= 1u;
+        } else {
+            ++stage;
+        }
     }
     // pixels whose transmittance came within the guard band of the floor: the last value
     // (the first below the floor, or the final one) and, for a pixel that crossed, the value
@@ -443,8 +568,7 @@ render_fwd_kernel(KParams kp, const float4* __restrict__ recs, const float4* __r
     const unsigned nexact = __reduce_add_sync(kFull, px.nexact);
     nfloor = __reduce_add_sync(kFull, nfloor);
     if (lane == 0) {
-        surv_count[tile * kWarpsPerCta + warp] = nsurv;
-        atomicAdd(counters + CNT_SURVIVORS, (unsigned long long)nsurv);
+        stream_used[tile * kBlocksPerTile + warp] = used;  // entries composited: all the backward needs
         if (nexact) atomicAdd(counters + CNT_EXACT, (unsigned long long)nexact);
         if (nfloor) atomicAdd(counters + CNT_TFLOOR, (unsigned long long)nfloor);
     }
@@ -453,24 +577,23 @@ render_fwd_kernel(KParams kp, const float4* __restrict__ recs, const float4* __r
 // ----------------------------------------------------------------- backward
 //
 // One CTA of 4 warps per HALF tile (16x8 pixels); a warp owns an 8x4 block as in
-// the forward.  The list is walked back to front in two sweeps per batch of
-// kBwdBatch queued survivors:
+// the forward and walks the part of its stream the forward composited, from the
+// back, in two sweeps per batch of kBwdBatch entries:
 //   sweep 1 (lane = pixel): the reverse compositing chain of rasterizer.cpp:
-//       189-213; per (pixel, survivor) it leaves three numbers in a padded
+//       189-213; per (pixel, entry) it leaves three numbers in a padded
 //       shared-memory matrix: wgt = alpha * T_before (colour gradient weight),
 //       y = d_alpha * w (opacity gradient term), z = d_alpha * o * dw/dm (the
 //       common factor of the conic and mean gradients), the last two gated by
 //       the alpha clamp;
-//   sweep 2 (lane = survivor x half of the pixels): each lane sums its
-//       survivor's nine gradients over 16 pixels in registers; one shuffle
-//       folds the two halves.  No per-survivor cross-lane reduction.
-// Then one red.global.add per gradient component per survivor.
+//   sweep 2 (lane = entry x half of the pixels): each lane sums its entry's nine
+//       gradients over 16 pixels in registers; one shuffle folds the two halves.
+//       No per-entry cross-lane reduction.
+// Then two 128-bit and one 32-bit red.global.add per entry into gradient rows
+// padded to 12 floats.
 constexpr int kBwdWarps = 4;
 constexpr int kBwdThreads = 32 * kBwdWarps;
 constexpr int kBwdBatch = 16;
 constexpr int kXStride = kBwdBatch + 1;  // odd: conflict-free both by row and by column
-constexpr int kBwdQueueCap = 48;         // 32 appended per chunk on top of at most kBwdBatch - 1 left over
-// per warp: queue, staging ring, 32 pixel gradients, three 32 x kXStride exchange matrices
 constexpr int kSplatGradStride = 12;     // internal gradient rows are padded to 12 floats for 128-bit atomics
 
 struct BwdPixel {
@@ -533,12 +656,12 @@ __device__ __forceinline__ void bwd_visit(const KParams& kp, const float4* __res
 template <int FAM>
 __global__ void __launch_bounds__(kBwdThreads, 4)
 render_bwd_kernel(KParams kp, const float4* __restrict__ recs, const int2* __restrict__ ranges,
-                  const float4* __restrict__ surv, size_t surv_stride,
-                  const int* __restrict__ surv_count, int W, int H, int tiles_x, float bg0, float bg1,
-                  float bg2, const float* __restrict__ grad_image,
+                  const float4* __restrict__ streams, const int* __restrict__ stream_used, int W, int H,
+                  int tiles_x, float bg0, float bg1, float bg2, const float* __restrict__ grad_image,
                   const float* __restrict__ t_final, const int* __restrict__ processed,
                   float* __restrict__ grads, unsigned long long* __restrict__ counters) {
-    __shared__ float4 queue[kBwdWarps][kBwdQueueCap * 3];
+    __shared__ __align__(128) float4 ring[kBwdWarps][kStages][kChunkVecs];
+    __shared__ unsigned long long bars[kBwdWarps][kStages];
     __shared__ float xch[kBwdWarps][3][32 * kXStride];
     __shared__ float4 gpix[kBwdWarps][32];
     const int tile = blockIdx.x >> 1, half = blockIdx.x & 1;
@@ -566,78 +689,71 @@ render_bwd_kernel(KParams kp, const float4* __restrict__ recs, const int2* __res
         px.T = t_final[p];
         px.nproc = processed[p];
     }
-    const int wmax = __reduce_max_sync(kFull, px.nproc);
-    if (wmax == 0) return;
+    if (__reduce_max_sync(kFull, px.nproc) == 0) return;
     px.s = (px.g0 * bg0 + px.g1 * bg1 + px.g2 * bg2) * px.T;
 
-    float4* q = queue[warp];
     float4* gp = gpix[warp];
     float* xw = xch[warp][0];
     float* xy = xch[warp][1];
     float* xz = xch[warp][2];
     gp[lane] = make_float4(px.g0, px.g1, px.g2, 0.f);
-    const unsigned lt_mask = (1u << lane) - 1u;
-    int head = 0, qn = 0;
 
-    // sweep-2 role of this lane: survivor sj of the batch, pixels [16 sh, 16 sh + 16)
+    // sweep-2 role of this lane: entry sj of the batch, pixels [16 sh, 16 sh + 16)
     const int sj = lane & (kBwdBatch - 1), sh = lane >> 4;
     const float* rw = xw + (sh * 16) * kXStride + sj;
     const float* ry = xy + (sh * 16) * kXStride + sj;
     const float* rz = xz + (sh * 16) * kXStride + sj;
     const float4* rg = gp + sh * 16;
     const float ex0 = X0, ey0 = Y0 + 2.f * sh;
+    float* ww = xw + lane * kXStride;
+    float* wy = xy + lane * kXStride;
+    float* wz = xz + lane * kXStride;
 
-    // The block's survivors, in the queue format the forward left them in, walked from the
-    // back: lane l of a chunk takes the l-th entry from the chunk's end, so lane order is
-    // descending list position and the loads are contiguous.  Entries the forward queued beyond
-    // the last position any of this block's pixels processed are dropped here.
-    const float4* sl = surv + survivor_list_offset(range.x, range.y, blk);
-    const int nsl = surv_count[tile * kWarpsPerCta + blk];
-    auto load_surv = [&](Entry& e, int k) {
-        if (k >= 0) {
-            e.v0 = __ldg(sl + k);
-            e.v1 = __ldg(sl + surv_stride + k);
-            e.v2 = __ldg(sl + 2 * surv_stride + k);
+    // The entries the forward composited, [0, used), chunk by chunk from the last.  Entries of the
+    // last batch beyond `used` (the stream is padded to a whole chunk) and entries past the last
+    // position a pixel processed are simply not eligible for that pixel.
+    const float4* src = streams + kEntryVecs * stream_offset(tile, range.x, range.y, blk);
+    const int used = stream_used[tile * kBlocksPerTile + blk];
+    const int nchunks = (used + kChunk - 1) / kChunk;
+    float4* stage0 = ring[warp][0];
+    unsigned long long* bar = bars[warp];
+    if (lane == 0) {
+        for (int s = 0; s < kStages; ++s) mbar_init(bar + s);
+        mbar_init_fence();
+        if (nchunks > 0) bulk_load(stage0, src + (size_t)(nchunks - 1) * kChunkVecs, kChunkBytes, bar);
+        if (nchunks > 1)
+            bulk_load(stage0 + kChunkVecs, src + (size_t)(nchunks - 2) * kChunkVecs, kChunkBytes, bar + 1);
+    }
+    __syncwarp();
+    int stage = 0;
+    unsigned parity = 0;
+    for (int c = nchunks - 1; c >= 0; --c) {
+        if (lane == 0 && c >= 2) {
+            const int fill = stage == 0 ? 2 : stage - 1;
+            bulk_load(stage0 + fill * kChunkVecs, src + (size_t)(c - 2) * kChunkVecs, kChunkBytes, bar + fill);
         }
-    };
-    Entry e;
-    load_surv(e, nsl - 1 - lane);
-    for (int top = nsl; top > 0; top -= 32) {
-        const bool survive = top - 1 - lane >= 0 && __float_as_int(e.v1.w) < wmax;
-        const unsigned mask = __ballot_sync(kFull, survive);
-        if (survive) {
-            int slot = head + qn + __popc(mask & lt_mask);
-            if (slot >= kBwdQueueCap) slot -= kBwdQueueCap;
-            q[slot * 3 + 0] = e.v0;
-            q[slot * 3 + 1] = e.v1;
-            q[slot * 3 + 2] = e.v2;
-        }
-        qn += __popc(mask);
-        load_surv(e, top - 33 - lane);
-        if (top <= 32) qn = queue_pad<kBwdQueueCap, kBwdBatch>(q, head, qn, lane);
-        while (qn >= kBwdBatch) {
-            const float4* qb = q + head * 3;
-            __syncwarp();
-            // ---- sweep 1: lane = pixel
-            float* ww = xw + lane * kXStride;
-            float* wy = xy + lane * kXStride;
-            float* wz = xz + lane * kXStride;
-            for (int j0 = 0; j0 < kBwdBatch; j0 += kGroup) {
+        mbar_wait(bar + stage, parity);
+        const float4* qc = stage0 + stage * kChunkVecs;
+        const int first = used - c * kChunk > kBwdBatch ? 1 : 0;  // upper batch holds composited entries?
+        for (int h = first; h >= 0; --h) {
+            const float4* qb = qc + h * (kBwdBatch * kEntryVecs);
+            // ---- sweep 1: lane = pixel, entries in descending list position
+            for (int j0 = kBwdBatch - kGroup; j0 >= 0; j0 -= kGroup) {
                 const BwdPixel save = px;
                 bool near_acc = false;
 #pragma unroll
-                for (int j = 0; j < kGroup; ++j)
+                for (int j = kGroup - 1; j >= 0; --j)
                     bwd_visit<FAM, false>(kp, recs, qb + (j0 + j) * 3, fx, fy, px, ww + j0 + j, wy + j0 + j,
                                           wz + j0 + j, near_acc);
                 if (kp.exact && __any_sync(kFull, near_acc)) {  // a few groups per thousand
                     px = save;
-                    for (int j = 0; j < kGroup; ++j)
+                    for (int j = kGroup - 1; j >= 0; --j)
                         bwd_visit<FAM, true>(kp, recs, qb + (j0 + j) * 3, fx, fy, px, ww + j0 + j, wy + j0 + j,
                                              wz + j0 + j, near_acc);
                 }
             }
             __syncwarp();
-            // ---- sweep 2: lane = (survivor, half of the pixels)
+            // ---- sweep 2: lane = (entry, half of the pixels)
             {
                 const float4 r0 = qb[sj * 3 + 0];
                 const float4 r1 = qb[sj * 3 + 1];
@@ -664,7 +780,7 @@ render_bwd_kernel(KParams kp, const float4* __restrict__ recs, const int2* __res
                     sx += zx;
                     sy += zy;
                 }
-                // fold the two pixel halves (lanes l and l ^ 16 hold the same survivor)
+                // fold the two pixel halves (lanes l and l ^ 16 hold the same entry)
                 dc0 += __shfl_xor_sync(kFull, dc0, 16);
                 dc1 += __shfl_xor_sync(kFull, dc1, 16);
                 dc2 += __shfl_xor_sync(kFull, dc2, 16);
@@ -687,8 +803,13 @@ render_bwd_kernel(KParams kp, const float4* __restrict__ recs, const int2* __res
                     atomicAdd(dst + 8, -fmaf(r0.w, sx, 2.f * r1.x * sy));
                 }
             }
-            head = head + kBwdBatch == kBwdQueueCap ? 0 : head + kBwdBatch;
-            qn -= kBwdBatch;
+            __syncwarp();
+        }
+        if (stage == kStages - 1) {
+            stage = 0;
+            parity ^= 1u;
+        } else {
+            ++stage;
         }
     }
     const unsigned nexact = __reduce_add_sync(kFull, px.nexact);
@@ -772,14 +893,19 @@ darbs_status launch_pack(darbs_cuda_ctx* ctx, const KParams& kp, int64_t n, cons
     return check_launch(ctx, "pack_kernel");
 }
 
-// Copies the records of the K sorted list entries into list order (see load_entry).
-darbs_status launch_gather(darbs_cuda_ctx* ctx) {
-    const int64_t k = ctx->fwd_entries;
-    DARBS_TRY(reserve(ctx, ctx->stream_recs, sizeof(float4) * 3 * (size_t)(k > 0 ? k : 1)));
-    if (k == 0) return DARBS_OK;
-    gather_kernel<<<(unsigned)((k + 255) / 256), 256, 0, ctx->stream>>>(
-        k, point_list_ptr(ctx), (const float4*)ctx->recs.ptr, (float4*)ctx->stream_recs.ptr);
-    return check_launch(ctx, "gather_kernel");
+// Tests every list entry against the eight blocks of its tile and writes the per-block
+// survivor streams the render kernels consume.
+darbs_status launch_cull(darbs_cuda_ctx* ctx, const KParams& kp) {
+    const int tiles = ctx->tiles_x * ctx->tiles_y;
+    if (tiles == 0) return DARBS_OK;
+    const size_t k = (size_t)(ctx->fwd_entries > 0 ? ctx->fwd_entries : 0);
+    const size_t entries = (size_t)kBlocksPerTile * (k + (size_t)kChunk * (size_t)tiles);
+    DARBS_TRY(reserve(ctx, ctx->streams, sizeof(float4) * kEntryVecs * entries));
+    DARBS_TRY(reserve(ctx, ctx->stream_count, sizeof(int) * 2 * kBlocksPerTile * (size_t)tiles));
+    cull_kernel<<<tiles, kThreads, 0, ctx->stream>>>(
+        kp, (const float4*)ctx->recs.ptr, (const int2*)ctx->ranges.ptr, point_list_ptr(ctx), ctx->tiles_x,
+        (float4*)ctx->streams.ptr, (int*)ctx->stream_count.ptr, (unsigned long long*)ctx->counters.ptr);
+    return check_launch(ctx, "cull_kernel");
 }
 
 darbs_status launch_render_fwd(darbs_cuda_ctx* ctx, const KParams& kp, int width, int height,
@@ -787,22 +913,16 @@ darbs_status launch_render_fwd(darbs_cuda_ctx* ctx, const KParams& kp, int width
                                int32_t* processed, int32_t* contributors) {
     int tiles = ctx->tiles_x * ctx->tiles_y;
     if (tiles == 0) return DARBS_OK;
-    // per-block survivor streams for the backward pass: 8 regions per tile, each as long as the
-    // tile's list (address space only; the forward writes survivors, a quarter of it or less)
-    const size_t k = (size_t)(ctx->fwd_entries > 0 ? ctx->fwd_entries : 1);
-    const size_t surv_stride = kWarpsPerCta * k;
-    DARBS_TRY(reserve(ctx, ctx->surv, sizeof(float4) * 3 * surv_stride));
-    DARBS_TRY(reserve(ctx, ctx->surv_count, sizeof(int) * kWarpsPerCta * (size_t)tiles));
-    ctx->surv_stride = (int64_t)surv_stride;
     auto* counters = (unsigned long long*)ctx->counters.ptr;
     const float4* recs = (const float4*)ctx->recs.ptr;
     const int2* ranges = (const int2*)ctx->ranges.ptr;
     const int* plist = point_list_ptr(ctx);
+    const int* count = (const int*)ctx->stream_count.ptr;
+    int* used = (int*)ctx->stream_count.ptr + (size_t)kBlocksPerTile * tiles;
 #define DARBS_LAUNCH_FWD(F)                                                                       \
     render_fwd_kernel<F><<<tiles, kThreads, 0, ctx->stream>>>(                                    \
-        kp, recs, (const float4*)ctx->stream_recs.ptr, k, ranges, plist, width, height,           \
-        ctx->tiles_x, bg[0], bg[1], bg[2], image, t_final, processed, contributors,               \
-        (float4*)ctx->surv.ptr, surv_stride, (int*)ctx->surv_count.ptr, counters)
+        kp, recs, ranges, plist, (const float4*)ctx->streams.ptr, count, used, width, height,     \
+        ctx->tiles_x, bg[0], bg[1], bg[2], image, t_final, processed, contributors, counters)
     switch (kp.fam) {
         case FAM_GAUSS2: DARBS_LAUNCH_FWD(FAM_GAUSS2); break;
         case FAM_HCOS2: DARBS_LAUNCH_FWD(FAM_HCOS2); break;
@@ -827,11 +947,11 @@ darbs_status launch_render_bwd(darbs_cuda_ctx* ctx, const KParams& kp, int width
     auto* counters = (unsigned long long*)ctx->counters.ptr;
     const float4* recs = (const float4*)ctx->recs.ptr;
     const int2* ranges = (const int2*)ctx->ranges.ptr;
+    const int* used = (const int*)ctx->stream_count.ptr + (size_t)kBlocksPerTile * tiles;
 #define DARBS_LAUNCH_BWD(F)                                                                       \
     render_bwd_kernel<F><<<2 * tiles, kBwdThreads, 0, ctx->stream>>>(                             \
-        kp, recs, ranges, (const float4*)ctx->surv.ptr, (size_t)ctx->surv_stride,                 \
-        (const int*)ctx->surv_count.ptr, width, height, ctx->tiles_x, bg[0], bg[1], bg[2],        \
-        grad_image, t_final, processed, (float*)ctx->splat_grads.ptr, counters)
+        kp, recs, ranges, (const float4*)ctx->streams.ptr, used, width, height, ctx->tiles_x,     \
+        bg[0], bg[1], bg[2], grad_image, t_final, processed, (float*)ctx->splat_grads.ptr, counters)
     switch (kp.fam) {
         case FAM_GAUSS2: DARBS_LAUNCH_BWD(FAM_GAUSS2); break;
         case FAM_HCOS2: DARBS_LAUNCH_BWD(FAM_HCOS2); break;
