@@ -242,7 +242,8 @@ DARBS_API darbs_status darbs_cuda_stage_times(darbs_cuda_ctx* ctx, double out_ms
 /* Work counters of the last forward: out[0] = K tile entries, out[1] = sum of
  * processed (visits), out[2] = sum of contributors, out[3] = (8x4 pixel block,
  * entry) pairs that survived the block-level cull, out[4] = FP64 guard-band
- * re-decisions, out[5] = pixels flagged near the transmittance floor.
+ * re-decisions, out[5] = pixels flagged near the transmittance floor, out[6] =
+ * (block, entry) pairs the forward composited before its early exits.
  * Synchronises. */
 DARBS_API darbs_status darbs_cuda_work_counters(darbs_cuda_ctx* ctx, int64_t out[8]);
 

@@ -288,7 +288,7 @@ class Context:
     def work_counters(self) -> dict:
         out = (C.c_int64 * 8)()
         self._check(_lib.darbs_cuda_work_counters(self._h, out))
-        names = ["entries", "visits", "contributors", "survivors", "exact", "tfloor"]
+        names = ["entries", "visits", "contributors", "survivors", "exact", "tfloor", "composited"]
         return {k: int(out[i]) for i, k in enumerate(names)}
 
     # -------------------------------------------------------------- kernel

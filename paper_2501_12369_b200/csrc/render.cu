@@ -42,7 +42,8 @@ constexpr unsigned kFull = 0xffffffffu;
 
 // counters (u64 each): 3 = surviving (block, entry) pairs, 4 = FP64 re-decisions,
 // 5 = pixels whose transmittance came within the guard band of the floor.
-enum { CNT_SURVIVORS = 3, CNT_EXACT = 4, CNT_TFLOOR = 5 };
+// 6 = (block, entry) pairs the forward composited (before its early exits cut the streams short).
+enum { CNT_SURVIVORS = 3, CNT_EXACT = 4, CNT_TFLOOR = 5, CNT_COMPOSITED = 6 };
 
 // ------------------------------------------------------------------ packing
 __global__ void pack_kernel(KParams kp, int64_t n, const float* __restrict__ mu2,
@@ -569,6 +570,7 @@ render_fwd_kernel(KParams kp, const float4* __restrict__ recs, const int2* __res
     nfloor = __reduce_add_sync(kFull, nfloor);
     if (lane == 0) {
         stream_used[tile * kBlocksPerTile + warp] = used;  // entries composited: all the backward needs
+        atomicAdd(counters + CNT_COMPOSITED, (unsigned long long)used);
         if (nexact) atomicAdd(counters + CNT_EXACT, (unsigned long long)nexact);
         if (nfloor) atomicAdd(counters + CNT_TFLOOR, (unsigned long long)nfloor);
     }
