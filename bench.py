@@ -251,6 +251,7 @@ def run_ours(args):
             params=torch.from_numpy(init).to(dev).clone(), m=torch.zeros(14 * n, device=dev),
             v=torch.zeros(14 * n, device=dev), grads=torch.zeros((n, 14), device=dev), target=target,
             target_host=target.cpu().pin_memory(), t=0)
+        state[name]["target_np"] = state[name]["target_host"].numpy()
     torch.cuda.synchronize()
 
     def iteration(name, e2e: bool):
@@ -259,9 +260,12 @@ def run_ours(args):
         s["grads"].zero_()
         if e2e:
             # the view's target image comes from pinned host memory through the C ABI
-            # (image_space = DARBS_HOST), the loss is read back to the host
-            loss = ctx.evaluate_view(k, psi, s["params"], cam, bg, target=s["target_host"].numpy(), lam=0.0,
-                                     param_grads=s["grads"])
+            # (image_space = DARBS_HOST); the loss of every iteration is read back to the host, one
+            # iteration late (darbs_cuda_pop_loss) so that the read-back never drains the stream
+            loss = ctx.evaluate_view(k, psi, s["params"], cam, bg, target=s["target_np"], lam=0.0,
+                                     param_grads=s["grads"], want_loss=False)
+            # the next iteration's target starts its upload under this iteration's render kernels
+            ctx.prefetch_target(state[KERNELS[(KERNELS.index(name) + 1) % len(KERNELS)]]["target_np"])
         else:
             loss = ctx.evaluate_view(k, psi, s["params"], cam, bg, target=s["target"], lam=0.0,
                                      param_grads=s["grads"], want_loss=False)
@@ -269,7 +273,19 @@ def run_ours(args):
             dist.all_reduce(s["grads"], op=dist.ReduceOp.SUM)  # gradients are summed over views, fit3d.cpp:148-158
         s["t"] += 1
         ctx.adam_step(s["params"].view(-1), s["grads"].view(-1), s["m"], s["v"], lrs, s["t"])
+        if e2e:
+            pending[0] += 1
+            if pending[0] > 1:  # the previous iteration's loss, now that this one is queued
+                losses.append(ctx.pop_loss())
+                pending[0] -= 1
         return loss
+
+    pending, losses = [0], []
+
+    def drain_losses():
+        while pending[0] > 0:
+            losses.append(ctx.pop_loss())
+            pending[0] -= 1
 
     def barrier():
         if world > 1:
@@ -278,24 +294,27 @@ def run_ours(args):
 
     def timed(steps, e2e):
         """K steps (each = one iteration per kernel), CUDA events on the launching stream."""
-        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in KERNELS]
+        ev = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in KERNELS]
+              for _ in range(steps)]
         per = {name: 0.0 for name in KERNELS}
         barrier()
         l0 = ctx.launch_count()
         t_start = torch.cuda.Event(enable_timing=True)
         t_end = torch.cuda.Event(enable_timing=True)
         t_start.record()
-        for _ in range(steps):
-            for (a, b), name in zip(ev, KERNELS):
+        for step in range(steps):  # no synchronisation between steps: the host runs ahead of the GPU
+            for (a, b), name in zip(ev[step], KERNELS):
                 a.record()
                 iteration(name, e2e)
                 b.record()
-            torch.cuda.synchronize()
-            for (a, b), name in zip(ev, KERNELS):
-                per[name] += a.elapsed_time(b)
+        if e2e:
+            drain_losses()  # inside the timed region: every iteration's loss has reached the host
         t_end.record()
         barrier()
         ms = t_start.elapsed_time(t_end)
+        for step in range(steps):
+            for (a, b), name in zip(ev[step], KERNELS):
+                per[name] += a.elapsed_time(b)
         if world > 1:
             t = torch.tensor([ms], device=dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -316,6 +335,8 @@ def run_ours(args):
     # end-to-end: target image from pinned host memory each iteration, loss read back
     for name in KERNELS:
         iteration(name, True)
+    drain_losses()
+    losses.clear()
     ms_e2e, per_e2e, _ = timed(args.steps, e2e=True)
     clocks = sampler.stop() if rank == 0 else None
     e2e_value = len(KERNELS) * args.steps * world / (ms_e2e * 1e-3)
@@ -428,7 +449,10 @@ def run_ours(args):
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": len(KERNELS) * 12 * w * h,
                 "d2h_bytes_per_step": len(KERNELS) * 32,
                 "path": "darbs_cuda_evaluate_view with the view's target image in pinned host memory "
-                        "(image_space = DARBS_HOST) and the loss read back; parameters stay on the device"},
+                        "(image_space = DARBS_HOST; darbs_cuda_prefetch_target starts each upload on a second "
+                        "stream under the previous iteration's render kernels) and every "
+                        "iteration's loss read back with darbs_cuda_pop_loss one iteration late; parameters "
+                        "stay on the device", "losses_read": len(losses)},
         "gpu_launches": int(launches),
         "roofline": roofline,
         "exact_decisions": bool(args.exact),

@@ -213,7 +213,9 @@ DARBS_API darbs_status darbs_cuda_backward_projection(darbs_cuda_ctx* ctx, doubl
  * DARBS_INVALID_PARAMETER.  image_out (may be NULL) receives the rendered view.
  * background: fit_scene uses (0,0,0) (fit3d.cpp:52).
  * Returns NUMERIC_ERROR when every primitive is culled (fit3d.cpp:117-119) or
- * the loss is not finite (fit3d.cpp:123-125); those checks synchronise. */
+ * the loss is not finite (fit3d.cpp:123-125); those checks need the results on the
+ * host: with loss_out they synchronise here, with loss_out == NULL they are
+ * reported by darbs_cuda_pop_loss. */
 DARBS_API darbs_status darbs_cuda_evaluate_view(darbs_cuda_ctx* ctx,
                                                 const darbs_kernel_spec* kernel, double psi,
                                                 int64_t n, const float* raw_params,
@@ -223,6 +225,22 @@ DARBS_API darbs_status darbs_cuda_evaluate_view(darbs_cuda_ctx* ctx,
                                                 float* image_out, double loss_out[4],
                                                 darbs_space param_space,
                                                 darbs_space image_space);
+
+/* Starts the upload of a view's target image (host memory, pinned for a truly asynchronous copy;
+ * count = 3*w*h floats) ahead of the darbs_cuda_evaluate_view call that will pass the same
+ * pointer as `target` with image_space = DARBS_HOST.  The transfer is queued on the context's
+ * copy stream behind the cull kernel of the last view queued, i.e. it runs under that view's
+ * render kernels.  Two uploads may be outstanding; the image must not change until its
+ * evaluate_view has been queued.  Without a prefetch evaluate_view uploads the image itself. */
+DARBS_API darbs_status darbs_cuda_prefetch_target(darbs_cuda_ctx* ctx, const float* host_image,
+                                                  int64_t count);
+
+/* Collects (total, l1, dssim, mse) and the status of the OLDEST darbs_cuda_evaluate_view that was
+ * called with loss_out == NULL (fit3d.cpp:117-125, :161-165), waiting only for that view's
+ * results.  Up to 4 views may be pending (older ones are forgotten); a training loop pops the loss of iteration i after it
+ * has queued iteration i + 1, so the GPU never idles on the read-back.  Passing loss_out to
+ * evaluate_view is the synchronous form (it drains everything pending). */
+DARBS_API darbs_status darbs_cuda_pop_loss(darbs_cuda_ctx* ctx, double loss_out[4]);
 
 /* adam_step, include/darbs/optim.hpp:24-39 (beta1 .9, beta2 .999, eps 1e-15,
  * per-parameter learning rates, t is 1-based). */

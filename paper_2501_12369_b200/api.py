@@ -96,6 +96,8 @@ def _load():
     lib.darbs_cuda_backward_projection.argtypes = [vp, dbl, i64, vp, vp, vp, C.POINTER(dbl), vp, vp, vp, i32]
     lib.darbs_cuda_evaluate_view.argtypes = [vp, ks, dbl, i64, vp, C.POINTER(dbl), C.POINTER(C.c_float), vp,
                                              dbl, vp, vp, vp, C.POINTER(dbl), i32, i32]
+    lib.darbs_cuda_pop_loss.argtypes = [vp, C.POINTER(dbl)]
+    lib.darbs_cuda_prefetch_target.argtypes = [vp, vp, i64]
     lib.darbs_cuda_microbench.argtypes = [vp, C.POINTER(dbl)]
     lib.darbs_cuda_adam_step.argtypes = [vp, i64, vp, vp, vp, vp, vp, i32, i32]
     lib.darbs_cuda_set_stage_timing.argtypes = [vp, i32]
@@ -111,7 +113,7 @@ EXPORTED_SYMBOLS = (
     "darbs_cuda_synchronize darbs_cuda_launch_count darbs_cuda_set_exact_decisions darbs_cuda_make_kernel "
     "darbs_cuda_kernel_preset darbs_cuda_default_psi darbs_cuda_eval darbs_cuda_bin darbs_cuda_forward "
     "darbs_cuda_backward darbs_cuda_realize darbs_cuda_project darbs_cuda_backward_projection "
-    "darbs_cuda_evaluate_view darbs_cuda_adam_step darbs_cuda_set_stage_timing darbs_cuda_stage_times "
+    "darbs_cuda_evaluate_view darbs_cuda_prefetch_target darbs_cuda_pop_loss darbs_cuda_adam_step darbs_cuda_set_stage_timing darbs_cuda_stage_times "
     "darbs_cuda_work_counters darbs_cuda_microbench"
 ).split()
 
@@ -430,6 +432,18 @@ class Context:
         self._check(_lib.darbs_cuda_evaluate_view(self._h, C.byref(kernel), psi, n, p_raw, pcam, bg, p_t, lam,
                                                   p_g, p_pg, p_img, loss if want_loss else None, a.space,
                                                   ai.space if ai.space is not None else a.space))
+        return tuple(float(x) for x in loss)
+
+    def prefetch_target(self, host_image):
+        """Start uploading a (pinned) host target image for a later evaluate_view(target=host_image)."""
+        if not (isinstance(host_image, np.ndarray) and host_image.dtype == np.float32 and host_image.flags.c_contiguous):
+            raise TypeError("prefetch_target needs a contiguous float32 numpy array (same object as the later target)")
+        self._check(_lib.darbs_cuda_prefetch_target(self._h, C.c_void_p(host_image.ctypes.data), host_image.size))
+
+    def pop_loss(self):
+        """(total, l1, dssim, mse) of the oldest evaluate_view called with want_loss=False."""
+        loss = (C.c_double * 4)()
+        self._check(_lib.darbs_cuda_pop_loss(self._h, loss))
         return tuple(float(x) for x in loss)
 
     def adam_step(self, params, grads, m, v, lrs, t: int):

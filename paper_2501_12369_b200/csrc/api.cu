@@ -208,7 +208,7 @@ struct Stager {
         return DARBS_OK;
     }
     darbs_status finish() {
-        if (space == DARBS_DEVICE) return DARBS_OK;
+        if (space == DARBS_DEVICE || npending == 0) return DARBS_OK;
         for (int i = 0; i < npending; ++i)
             DARBS_CUDA_TRY(ctx, cudaMemcpyAsync(pending[i].host, pending[i].dev, pending[i].bytes,
                                                 cudaMemcpyDeviceToHost, ctx->stream));
@@ -267,6 +267,10 @@ darbs_status forward_device(darbs_cuda_ctx* ctx, const KParams& kp, int64_t n, c
         DARBS_TRY(launch_pack(ctx, kp, n, mu2, conic, opacity, rgb));
         DARBS_TRY(launch_cull(ctx, kp));
     }
+    // prefetched uploads may start here: from now on the stream holds a few long kernels, whose
+    // launches a bulk PCIe transfer cannot delay (it does delay the many short ones of the sort)
+    cudaEventRecord(ctx->after_cull, ctx->stream);
+    ctx->have_after_cull = true;
     DARBS_TRY(reserve(ctx, ctx->t_final, sizeof(float) * (px ? px : 1)));
     DARBS_TRY(reserve(ctx, ctx->processed, sizeof(int32_t) * (px ? px : 1)));
     if (!image) {
@@ -330,6 +334,12 @@ darbs_status darbs_cuda_create(int device, darbs_cuda_ctx** out_ctx) {
     cudaEventCreateWithFlags(&ctx->copy_done, cudaEventDisableTiming);
     for (int i = 0; i < 16; ++i) cudaEventCreate(&ctx->timer.ev[i]);
     ctx->timer.created = true;
+    cudaEventCreateWithFlags(&ctx->after_cull, cudaEventDisableTiming);
+    for (int i = 0; i < 2; ++i) cudaEventCreateWithFlags(&ctx->target_done[i], cudaEventDisableTiming);
+    for (int i = 0; i < kLossRing; ++i) {
+        cudaMallocHost(&ctx->loss_ring[i].host, 64);
+        cudaEventCreateWithFlags(&ctx->loss_ring[i].done, cudaEventDisableTiming);
+    }
     darbs_status st = reserve(ctx, ctx->counters, 256);
     if (st == DARBS_OK) st = reserve_pinned(ctx, 256);
     if (st == DARBS_OK && cudaMemsetAsync(ctx->counters.ptr, 0, 256, ctx->stream) != cudaSuccess)
@@ -360,6 +370,15 @@ void darbs_cuda_destroy(darbs_cuda_ctx* ctx) {
     if (ctx->pinned) cudaFreeHost(ctx->pinned);
     if (ctx->timer.created)
         for (int i = 0; i < 16; ++i) cudaEventDestroy(ctx->timer.ev[i]);
+    for (int i = 0; i < kLossRing; ++i) {
+        if (ctx->loss_ring[i].host) cudaFreeHost(ctx->loss_ring[i].host);
+        if (ctx->loss_ring[i].done) cudaEventDestroy(ctx->loss_ring[i].done);
+    }
+    if (ctx->after_cull) cudaEventDestroy(ctx->after_cull);
+    for (int i = 0; i < 2; ++i) {
+        if (ctx->target_done[i]) cudaEventDestroy(ctx->target_done[i]);
+        if (ctx->target_stage[i].ptr) cudaFree(ctx->target_stage[i].ptr);
+    }
     if (ctx->copy_begin) cudaEventDestroy(ctx->copy_begin);
     if (ctx->copy_done) cudaEventDestroy(ctx->copy_done);
     if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
@@ -700,7 +719,16 @@ darbs_status darbs_cuda_evaluate_view(darbs_cuda_ctx* ctx, const darbs_kernel_sp
     const float *d_raw, *d_target, *d_gimg;
     float *d_pgrads, *d_image;
     DARBS_TRY(st.in(raw_params, 14 * nn, &d_raw));
-    DARBS_TRY(sti.in_late(target, 3 * px, &d_target));  // not needed before the loss: overlaps the forward
+    int staged = -1;
+    if (target && image_space == DARBS_HOST)
+        for (int i = 0; i < 2; ++i)
+            if (ctx->target_src[i] == target && ctx->target_stage[i].bytes >= sizeof(float) * 3 * px) staged = i;
+    if (staged >= 0) {
+        d_target = (const float*)ctx->target_stage[staged].ptr;  // uploaded by darbs_cuda_prefetch_target
+        ctx->target_src[staged] = nullptr;
+    } else {
+        DARBS_TRY(sti.in_late(target, 3 * px, &d_target));  // not needed before the loss: overlaps the forward
+    }
     DARBS_TRY(sti.in(grad_image, 3 * px, &d_gimg));
     DARBS_TRY(st.inout(param_grads, 14 * nn, &d_pgrads));
     DARBS_TRY(sti.out(image_out, 3 * px, &d_image));
@@ -730,6 +758,7 @@ darbs_status darbs_cuda_evaluate_view(darbs_cuda_ctx* ctx, const darbs_kernel_sp
     DARBS_TRY(forward_device(ctx, kp, n, d_mu2, d_conic, d_radius, d_depth, d_opacity, d_rgb, d_valid,
                              width, height, background, d_image, nullptr));
     DARBS_TRY(sti.await_late());
+    if (staged >= 0) DARBS_CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->stream, ctx->target_done[staged], 0));
     if (target) {
         StageScope ts(ctx, ST_LOSS);
         DARBS_TRY(reserve(ctx, ctx->grad_image, sizeof(float) * 3 * px));
@@ -751,25 +780,74 @@ darbs_status darbs_cuda_evaluate_view(darbs_cuda_ctx* ctx, const darbs_kernel_sp
     }
     DARBS_TRY(st.finish());
     DARBS_TRY(sti.finish());
-    if (loss_out) {
-        // flags (2 ints) and loss sums (2 doubles) in one pinned read
-        DARBS_CUDA_TRY(ctx, cudaMemcpyAsync(ctx->pinned, d_flags, 32, cudaMemcpyDeviceToHost, ctx->stream));
-        DARBS_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
-        const int* flags = (const int*)ctx->pinned;
-        const double* sums = (const double*)((const char*)ctx->pinned + 16);
-        loss_out[0] = loss_out[1] = loss_out[2] = loss_out[3] = 0.0;
-        if (target) {
-            double cnt = (double)(3 * px);
-            loss_out[1] = sums[0] / cnt;                    // l1      loss.cpp:188
-            loss_out[2] = 0.0;                              // dssim (lambda == 0: not evaluated)
-            loss_out[0] = (1.0 - lambda) * loss_out[1];     // total   loss.cpp:228
-            loss_out[3] = sums[1] / cnt;                    // mse     image.cpp mse()
-        }
-        if (flags[0] & 1) return fail(ctx, DARBS_INVALID_PARAMETER, "covariance_from_scale_rot: scale must be positive");
-        if (flags[0] & 2) return fail(ctx, DARBS_NUMERIC_ERROR, "conic_and_radius: covariance not positive definite");
-        if (flags[1] == 0) return fail(ctx, DARBS_NUMERIC_ERROR, "fit_scene: all primitives culled in one view");
-        if (target && !std::isfinite(loss_out[0])) return fail(ctx, DARBS_NUMERIC_ERROR, "fit_scene: loss diverged");
+    // flags (2 ints) and loss sums (2 doubles) travel to a pinned ring slot; the caller either waits
+    // for them now (loss_out) or collects them later with darbs_cuda_pop_loss, so that a training
+    // loop never has to drain the stream between two iterations
+    if (ctx->loss_pending == kLossRing) {  // nobody collects them: forget the oldest
+        ctx->loss_head = (ctx->loss_head + 1) % kLossRing;
+        --ctx->loss_pending;
     }
+    LossSlot& slot = ctx->loss_ring[(ctx->loss_head + ctx->loss_pending) % kLossRing];
+    slot.count = target ? (double)(3 * px) : 0.0;
+    slot.lambda = lambda;
+    DARBS_CUDA_TRY(ctx, cudaMemcpyAsync(slot.host, d_flags, 32, cudaMemcpyDeviceToHost, ctx->stream));
+    DARBS_CUDA_TRY(ctx, cudaEventRecord(slot.done, ctx->stream));
+    ++ctx->loss_pending;
+    if (loss_out) {
+        // the synchronous form: drain older pending losses, then this one
+        darbs_status st_last = DARBS_OK;
+        while (ctx->loss_pending > 0) st_last = darbs_cuda_pop_loss(ctx, loss_out);
+        return st_last;
+    }
+    return DARBS_OK;
+}
+
+darbs_status darbs_cuda_prefetch_target(darbs_cuda_ctx* ctx, const float* host_image, int64_t count) {
+    CTX_OR_FAIL(ctx);
+    if (!host_image || count <= 0) return fail(ctx, DARBS_INVALID_PARAMETER, "prefetch_target: empty image");
+    DeviceGuard guard(ctx->device);
+    const int slot = ctx->target_next;
+    ctx->target_next ^= 1;
+    ctx->target_src[slot] = nullptr;
+    DARBS_TRY(reserve(ctx, ctx->target_stage[slot], sizeof(float) * (size_t)count));
+    // behind the cull of the last view queued (its forward and backward kernels hide the transfer);
+    // that point is also past every reader of this slot, used two views ago
+    if (ctx->have_after_cull) {
+        DARBS_CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->copy_stream, ctx->after_cull, 0));
+    } else {
+        DARBS_CUDA_TRY(ctx, cudaEventRecord(ctx->copy_begin, ctx->stream));
+        DARBS_CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->copy_stream, ctx->copy_begin, 0));
+    }
+    DARBS_CUDA_TRY(ctx, cudaMemcpyAsync(ctx->target_stage[slot].ptr, host_image, sizeof(float) * (size_t)count,
+                                        cudaMemcpyHostToDevice, ctx->copy_stream));
+    DARBS_CUDA_TRY(ctx, cudaEventRecord(ctx->target_done[slot], ctx->copy_stream));
+    ctx->target_src[slot] = host_image;
+    return DARBS_OK;
+}
+
+darbs_status darbs_cuda_pop_loss(darbs_cuda_ctx* ctx, double loss_out[4]) {
+    CTX_OR_FAIL(ctx);
+    if (ctx->loss_pending == 0) return fail(ctx, DARBS_CONTRACT_VIOLATION, "pop_loss: no evaluate_view pending");
+    DeviceGuard guard(ctx->device);
+    LossSlot& slot = ctx->loss_ring[ctx->loss_head];
+    ctx->loss_head = (ctx->loss_head + 1) % kLossRing;
+    --ctx->loss_pending;
+    DARBS_CUDA_TRY(ctx, cudaEventSynchronize(slot.done));
+    const int* flags = (const int*)slot.host;
+    const double* sums = (const double*)((const char*)slot.host + 16);
+    double out[4] = {0.0, 0.0, 0.0, 0.0};
+    if (slot.count > 0.0) {
+        out[1] = sums[0] / slot.count;              // l1      loss.cpp:188
+        out[2] = 0.0;                               // dssim (lambda == 0: not evaluated)
+        out[0] = (1.0 - slot.lambda) * out[1];      // total   loss.cpp:228
+        out[3] = sums[1] / slot.count;              // mse     image.cpp mse()
+    }
+    if (loss_out)
+        for (int i = 0; i < 4; ++i) loss_out[i] = out[i];
+    if (flags[0] & 1) return fail(ctx, DARBS_INVALID_PARAMETER, "covariance_from_scale_rot: scale must be positive");
+    if (flags[0] & 2) return fail(ctx, DARBS_NUMERIC_ERROR, "conic_and_radius: covariance not positive definite");
+    if (flags[1] == 0) return fail(ctx, DARBS_NUMERIC_ERROR, "fit_scene: all primitives culled in one view");
+    if (slot.count > 0.0 && !std::isfinite(out[0])) return fail(ctx, DARBS_NUMERIC_ERROR, "fit_scene: loss diverged");
     return DARBS_OK;
 }
 

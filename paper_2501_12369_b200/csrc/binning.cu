@@ -82,10 +82,16 @@ __global__ void gather_touched_kernel(int64_t n, const unsigned* __restrict__ to
     if (r < n) touched_in_order[r] = touched[order[r]];
 }
 
+// K goes both to the device scalars and straight into pinned host memory (mapped under UVA): the
+// host needs it to size the tile sort, and a write from the SM does not queue behind a bulk
+// host <-> device copy that may be in flight on the copy engines.
 __global__ void total_kernel(int64_t n, const unsigned* __restrict__ offsets,
                              const unsigned* __restrict__ touched_in_order,
-                             Scalars* __restrict__ scalars) {
-    scalars->total_entries = (unsigned long long)offsets[n - 1] + touched_in_order[n - 1];
+                             Scalars* __restrict__ scalars, volatile unsigned long long* host_total) {
+    const unsigned long long k = (unsigned long long)offsets[n - 1] + touched_in_order[n - 1];
+    scalars->total_entries = k;
+    *host_total = k;
+    __threadfence_system();
 }
 
 __global__ void duplicate_kernel(int64_t n, const unsigned* __restrict__ order,
@@ -213,12 +219,11 @@ darbs_status run_binning(darbs_cuda_ctx* ctx, int64_t n, const float* mu2, const
     DARBS_CUDA_TRY(ctx, cub::DeviceScan::ExclusiveSum(ctx->cub_temp.ptr, scan_bytes, touched_in_order,
                                                      offsets, (int)n, s));
     ctx->launches += 2;
-    total_kernel<<<1, 1, 0, s>>>(n, offsets, touched_in_order, scalars);
-    DARBS_TRY(check_launch(ctx, "total_kernel"));
     DARBS_TRY(reserve_pinned(ctx, 64));
-    DARBS_CUDA_TRY(ctx, cudaMemcpyAsync(ctx->pinned, scalars, sizeof(Scalars), cudaMemcpyDeviceToHost, s));
+    total_kernel<<<1, 1, 0, s>>>(n, offsets, touched_in_order, scalars, (volatile unsigned long long*)ctx->pinned);
+    DARBS_TRY(check_launch(ctx, "total_kernel"));
     DARBS_CUDA_TRY(ctx, cudaStreamSynchronize(s));
-    const unsigned long long k = ((Scalars*)ctx->pinned)->total_entries;
+    const unsigned long long k = *(volatile unsigned long long*)ctx->pinned;
     if (k >= (1ull << 31)) return fail(ctx, DARBS_INVALID_PARAMETER, "more than 2^31 tile entries");
     ctx->fwd_entries = (int64_t)k;
     if (k == 0) return DARBS_OK;

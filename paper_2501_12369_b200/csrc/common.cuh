@@ -55,6 +55,16 @@ struct Counters {  // device-side, 8 x u64
     unsigned long long v[8];
 };
 
+// One evaluate_view whose loss has not been collected yet: the device -> host copy of its status
+// flags and loss sums lands in `host` (pinned) when `done` fires.
+static constexpr int kLossRing = 4;
+struct LossSlot {
+    void* host = nullptr;
+    cudaEvent_t done = nullptr;
+    double count = 0.0;   // number of image values, 0 when the view had no target
+    double lambda = 0.0;
+};
+
 struct StageTimer {
     cudaEvent_t ev[16];
     bool created = false;
@@ -97,6 +107,17 @@ struct darbs_cuda_ctx {
     darbs_b200::DeviceBuffer grad_image;   // 3wh
     void* pinned = nullptr;                // small pinned host scratch
     size_t pinned_bytes = 0;
+
+    // target images uploaded ahead of the evaluate_view that uses them (darbs_cuda_prefetch_target)
+    darbs_b200::DeviceBuffer target_stage[2];
+    const void* target_src[2] = {nullptr, nullptr};
+    cudaEvent_t target_done[2] = {nullptr, nullptr};
+    int target_next = 0;
+    cudaEvent_t after_cull = nullptr;  // the last forward's long kernels start here
+    bool have_after_cull = false;
+
+    darbs_b200::LossSlot loss_ring[darbs_b200::kLossRing];
+    int loss_head = 0, loss_pending = 0;
 
     // state of the last forward (the resident BlendAux)
     bool have_forward = false;
