@@ -209,7 +209,7 @@ DARBS_API darbs_status darbs_cuda_backward_projection(darbs_cuda_ctx* ctx, doubl
  *   target     [3wh]: loss_total(image, target, lambda) (src/loss.cpp:173-230)
  *                     drives the backward; *loss_out receives total, l1, dssim, mse.
  *   grad_image [3wh]: used as dL/dimage directly (loss_out gets zeros).
- * Only lambda == 0 (pure L1) is implemented in this round; other values return
+ * lambda in [0, 1] (fit_common.hpp:16 defaults to 0.2); other values return
  * DARBS_INVALID_PARAMETER.  image_out (may be NULL) receives the rendered view.
  * background: fit_scene uses (0,0,0) (fit3d.cpp:52).
  * Returns NUMERIC_ERROR when every primitive is culled (fit3d.cpp:117-119) or
@@ -242,6 +242,18 @@ DARBS_API darbs_status darbs_cuda_prefetch_target(darbs_cuda_ctx* ctx, const flo
  * evaluate_view is the synchronous form (it drains everything pending). */
 DARBS_API darbs_status darbs_cuda_pop_loss(darbs_cuda_ctx* ctx, double loss_out[4]);
 
+/* loss_total, src/loss.cpp:173-230 (LossResult, include/darbs/loss.hpp:7-12):
+ * L = (1 - lambda) L1 + lambda (1 - SSIM)/2 with the 11x11 sigma-1.5 window and mirror padding,
+ * and its analytic gradient with respect to `rendered`.  rendered, target, grad_image: [3wh],
+ * row-major RGB interleaved.  loss_out (host, may be NULL; synchronises when given) receives
+ * total, l1, dssim, mse; grad_image may be NULL (values only).  The reference throws
+ * invalid_parameter on a dimension mismatch (loss.cpp:174-176); here both images share the one
+ * (width, height) of the call. */
+DARBS_API darbs_status darbs_cuda_loss_total(darbs_cuda_ctx* ctx, int width, int height,
+                                             const float* rendered, const float* target,
+                                             double lambda, double loss_out[4], float* grad_image,
+                                             darbs_space space);
+
 /* adam_step, include/darbs/optim.hpp:24-39 (beta1 .9, beta2 .999, eps 1e-15,
  * per-parameter learning rates, t is 1-based). */
 DARBS_API darbs_status darbs_cuda_adam_step(darbs_cuda_ctx* ctx, int64_t dim, float* params,
@@ -270,7 +282,8 @@ DARBS_API darbs_status darbs_cuda_work_counters(darbs_cuda_ctx* ctx, int64_t out
  * per second with register operands (x2 = FLOP/s), out[1] = MUFU (ex2.approx)
  * operations per second, out[2] = SM clock in MHz seen by the FMA loop (clock64
  * span / event time), out[3] = number of SMs, out[4] = FP32 FMA instructions per
- * second in the immediate-operand form. */
+ * second in the immediate-operand form, out[5] = packed FP32 FMA instructions
+ * (fma.rn.f32x2, two FMAs per lane) per second. */
 DARBS_API darbs_status darbs_cuda_microbench(darbs_cuda_ctx* ctx, double out[8]);
 
 #ifdef __cplusplus

@@ -112,6 +112,10 @@ class Oracle:
         lib.darbs_cpu_param_grads.argtypes = [C.c_double, C.c_int, _ip, _dp, _dp, _dp, _dp, _dp, _dp, _dp]
         lib.darbs_cpu_param_grads.restype = None
         lib.darbs_cpu_adam_step.argtypes = [C.c_int64, _dp, _dp, _dp, _dp, _dp, C.c_int]
+        lib.darbs_cpu_loss_total.argtypes = [C.c_int, C.c_int, _dp, _dp, C.c_double, _dp, _dp]
+        lib.darbs_cpu_ssim.argtypes = [C.c_int, C.c_int, _dp, _dp, _dp]
+        lib.darbs_cpu_random_image.argtypes = [C.c_int, C.c_int, C.c_uint64, C.c_int, _dp]
+        lib.darbs_cpu_random_image.restype = None
 
     # ------------------------------------------------------------------ kernel
     @property
@@ -270,6 +274,29 @@ class Oracle:
         self.lib.darbs_cpu_param_grads(psi, owner.size, _i(owner), _d(sg), _d(conic), _d(opacity), _d(rgb),
                                        _d(prims), _d(cam), _d(out))
         return out
+
+    def random_image(self, width, height, seed, round_f32=True):
+        """tests/test_loss.cpp:13-19: U[0,1) per value from mt19937_64(seed); (h, w, 3)."""
+        img = np.empty((height, width, 3))
+        self.lib.darbs_cpu_random_image(width, height, seed, int(round_f32), _d(img))
+        return img
+
+    def loss_total(self, rendered, target, lam, want_grad=True):
+        """loss.cpp:173-230 -> (status, (total, l1, dssim), grad or None); images are (h, w, 3)."""
+        rendered, target = _f64(rendered), _f64(target)
+        h, w = rendered.shape[:2]
+        out = np.zeros(3)
+        grad = np.empty_like(rendered) if want_grad else None
+        st = self.lib.darbs_cpu_loss_total(w, h, _d(rendered), _d(target), float(lam), _d(out),
+                                           _d(grad) if want_grad else None)
+        return st, tuple(out), grad
+
+    def ssim(self, a, b):
+        a, b = _f64(a), _f64(b)
+        h, w = a.shape[:2]
+        out = np.zeros(1)
+        st = self.lib.darbs_cpu_ssim(w, h, _d(a), _d(b), _d(out))
+        return st, float(out[0])
 
     def adam_step(self, params, grads, m, v, lrs, t):
         params, grads, m, v, lrs = (_f64(a).copy() for a in (params, grads, m, v, lrs))

@@ -9,7 +9,7 @@
  *                               it follows; travels to the GPU box.
  *   oracle/_ref/libdarbs_ref.so the reference's OWN sources
  *                               (/root/reference/proj/core/src/{kernel,geometry,
- *                               rasterizer}.cpp, unmodified) compiled against
+ *                               rasterizer,loss}.cpp, unmodified) compiled against
  *                               oracle/eigen_shim and wrapped by
  *                               oracle/ref_glue.cpp.
  *
@@ -150,6 +150,17 @@ void darbs_cpu_backward_projection(double psi, int n, const double* grad_cov2,
 void darbs_cpu_param_grads(double psi, int m, const int32_t* owner, const double* splat_grads,
                            const double* conic, const double* opacity, const double* rgb,
                            const double* prims, const double* camera, double* param_grads);
+
+/* loss_total loss.cpp:173-230: L = (1 - lambda) L1 + lambda (1 - SSIM)/2 with its analytic gradient
+ * with respect to `rendered` (3*w*h, row-major RGB interleaved, like the images).  out[0..2] =
+ * total, l1, dssim.  grad may be NULL. */
+int darbs_cpu_loss_total(int width, int height, const double* rendered, const double* target,
+                         double lambda, double out[3], double* grad);
+/* ssim loss.cpp:142-171: mean SSIM over pixels and channels. */
+int darbs_cpu_ssim(int width, int height, const double* a, const double* b, double* out);
+/* The reference's random_image fixture (tests/test_loss.cpp:13-19): U[0,1) per value from
+ * std::mt19937_64(seed), optionally rounded to float32. */
+void darbs_cpu_random_image(int width, int height, uint64_t seed, int round_f32, double* rgb);
 
 /* adam_step optim.hpp:24-39 (t is 1-based). */
 int darbs_cpu_adam_step(int64_t dim, double* params, const double* grads, double* m, double* v,

@@ -614,6 +614,188 @@ void darbs_cpu_random_image_grad(int width, int height, uint64_t seed, int round
     for (size_t i = 0; i < n; ++i) grad_image[i] = rf(mt64_uniform(&g, -1.0, 1.0), round_f32);
 }
 
+void darbs_cpu_random_image(int width, int height, uint64_t seed, int round_f32, double* rgb) {
+    mt64 g;
+    mt64_seed(&g, seed);
+    size_t n = (size_t)width * height * 3;
+    for (size_t i = 0; i < n; ++i) rgb[i] = rf(mt64_uniform(&g, 0.0, 1.0), round_f32);
+}
+
+/* ------------------------------------------------------------------- loss */
+/* loss.cpp: 11-tap Gaussian window sigma 1.5 (:13-32), mirror padding (:35-41), separable
+ * moment filters (:47-74, :105-108), their adjoints (:76-103, :112-115), ssim_terms (:124-140),
+ * ssim (:144-171), loss_total (:173-230). */
+enum { LOSS_WIN = 11, LOSS_HALF = 5 };
+
+static const double* loss_window(void) { /* loss.cpp:19-32 */
+    static double w[LOSS_WIN];
+    static int ready = 0;
+    if (!ready) {
+        double sum = 0.0;
+        for (int i = 0; i < LOSS_WIN; ++i) {
+            double d = i - LOSS_HALF;
+            w[i] = exp(-d * d / (2.0 * 1.5 * 1.5));
+            sum += w[i];
+        }
+        for (int i = 0; i < LOSS_WIN; ++i) w[i] /= sum;
+        ready = 1;
+    }
+    return w;
+}
+
+static int loss_reflect(int i, int n) { /* loss.cpp:35-41 */
+    while (i < 0 || i >= n) {
+        if (i < 0) i = -i - 1;
+        if (i >= n) i = 2 * n - 1 - i;
+    }
+    return i;
+}
+
+/* filter_2d loss.cpp:105-108: rows first into tmp, then columns. */
+static void loss_filter2d(const double* in, double* out, double* tmp, int w, int h) {
+    const double* k = loss_window();
+    for (int y = 0; y < h; ++y)
+        for (int x = 0; x < w; ++x) {
+            double acc = 0.0;
+            for (int d = -LOSS_HALF; d <= LOSS_HALF; ++d)
+                acc += k[d + LOSS_HALF] * in[(size_t)y * w + loss_reflect(x + d, w)];
+            tmp[(size_t)y * w + x] = acc;
+        }
+    for (int x = 0; x < w; ++x)
+        for (int y = 0; y < h; ++y) {
+            double acc = 0.0;
+            for (int d = -LOSS_HALF; d <= LOSS_HALF; ++d)
+                acc += k[d + LOSS_HALF] * tmp[(size_t)loss_reflect(y + d, h) * w + x];
+            out[(size_t)y * w + x] = acc;
+        }
+}
+
+/* scatter_2d loss.cpp:112-115: the transposes in reverse order (columns, then rows). */
+static void loss_scatter2d(const double* in, double* out, double* tmp, int w, int h) {
+    const double* k = loss_window();
+    size_t np = (size_t)w * h;
+    for (size_t i = 0; i < np; ++i) tmp[i] = 0.0;
+    for (int y = 0; y < h; ++y)
+        for (int x = 0; x < w; ++x) {
+            double v = in[(size_t)y * w + x];
+            if (v == 0.0) continue;
+            for (int d = -LOSS_HALF; d <= LOSS_HALF; ++d)
+                tmp[(size_t)loss_reflect(y + d, h) * w + x] += k[d + LOSS_HALF] * v;
+        }
+    for (size_t i = 0; i < np; ++i) out[i] = 0.0;
+    for (int y = 0; y < h; ++y)
+        for (int x = 0; x < w; ++x) {
+            double v = tmp[(size_t)y * w + x];
+            if (v == 0.0) continue;
+            for (int d = -LOSS_HALF; d <= LOSS_HALF; ++d)
+                out[(size_t)y * w + loss_reflect(x + d, w)] += k[d + LOSS_HALF] * v;
+        }
+}
+
+/* ssim_terms loss.cpp:124-140 */
+static double loss_ssim_terms(double mu_x, double mu_y, double sxx, double syy, double sxy,
+                              double* d_mu_x, double* d_sxx, double* d_sxy) {
+    const double c1 = 0.01 * 0.01, c2 = 0.03 * 0.03;
+    double var_x = sxx - mu_x * mu_x;
+    double var_y = syy - mu_y * mu_y;
+    double cov = sxy - mu_x * mu_y;
+    double a1 = 2.0 * mu_x * mu_y + c1;
+    double a2 = 2.0 * cov + c2;
+    double b1 = mu_x * mu_x + mu_y * mu_y + c1;
+    double b2 = var_x + var_y + c2;
+    double denom = b1 * b2;
+    if (d_mu_x)
+        *d_mu_x = 2.0 * mu_y * (a2 - a1) / denom - 2.0 * mu_x * a1 * a2 * (b2 - b1) / (denom * denom);
+    if (d_sxx) *d_sxx = -a1 * a2 / (b1 * b2 * b2);
+    if (d_sxy) *d_sxy = 2.0 * a1 / denom;
+    return a1 * a2 / denom;
+}
+
+typedef struct {
+    double *x, *y, *buf, *tmp, *mu_x, *mu_y, *sxx, *syy, *sxy, *fa, *fb, *fd, *sa, *sb, *sd;
+    double* block;
+} loss_planes;
+
+static int loss_planes_alloc(loss_planes* p, size_t np) {
+    p->block = (double*)malloc(sizeof(double) * 15 * (np ? np : 1));
+    if (!p->block) return 0;
+    double** f = &p->x;
+    for (int i = 0; i < 15; ++i) f[i] = p->block + (size_t)i * np;
+    return 1;
+}
+
+/* moments of one channel, loss.cpp:150-163 / :206-216 */
+static void loss_moments(loss_planes* p, const double* a, const double* b, int c, int w, int h) {
+    size_t np = (size_t)w * h;
+    for (size_t i = 0; i < np; ++i) {
+        p->x[i] = a[i * 3 + c];
+        p->y[i] = b[i * 3 + c];
+    }
+    loss_filter2d(p->x, p->mu_x, p->tmp, w, h);
+    loss_filter2d(p->y, p->mu_y, p->tmp, w, h);
+    for (size_t i = 0; i < np; ++i) p->buf[i] = p->x[i] * p->x[i];
+    loss_filter2d(p->buf, p->sxx, p->tmp, w, h);
+    for (size_t i = 0; i < np; ++i) p->buf[i] = p->y[i] * p->y[i];
+    loss_filter2d(p->buf, p->syy, p->tmp, w, h);
+    for (size_t i = 0; i < np; ++i) p->buf[i] = p->x[i] * p->y[i];
+    loss_filter2d(p->buf, p->sxy, p->tmp, w, h);
+}
+
+int darbs_cpu_ssim(int width, int height, const double* a, const double* b, double* out) {
+    if (width < 0 || height < 0) return DARBS_CPU_INVALID_PARAMETER;
+    size_t np = (size_t)width * height;
+    loss_planes p;
+    if (!loss_planes_alloc(&p, np)) return DARBS_CPU_NUMERIC_ERROR;
+    double acc = 0.0;
+    for (int c = 0; c < 3; ++c) {
+        loss_moments(&p, a, b, c, width, height);
+        for (size_t i = 0; i < np; ++i)
+            acc += loss_ssim_terms(p.mu_x[i], p.mu_y[i], p.sxx[i], p.syy[i], p.sxy[i], NULL, NULL, NULL);
+    }
+    free(p.block);
+    *out = acc / (3.0 * (double)np);
+    return DARBS_CPU_OK;
+}
+
+int darbs_cpu_loss_total(int width, int height, const double* rendered, const double* target,
+                         double lambda, double out[3], double* grad) {
+    if (width < 0 || height < 0) return DARBS_CPU_INVALID_PARAMETER;
+    size_t np = (size_t)width * height, n = 3 * np;
+    loss_planes p;
+    if (!loss_planes_alloc(&p, np)) return DARBS_CPU_NUMERIC_ERROR;
+    double l1 = 0.0;
+    for (size_t i = 0; i < n; ++i) { /* loss.cpp:183-188 */
+        double d = rendered[i] - target[i];
+        l1 += fabs(d);
+        if (grad) grad[i] = (1.0 - lambda) * (double)((d > 0) - (d < 0)) / (double)n;
+    }
+    l1 /= (double)n;
+    double ssim_acc = 0.0;
+    const double scale = -0.5 * lambda / (double)n; /* loss.cpp:196 */
+    for (int c = 0; c < 3; ++c) {
+        loss_moments(&p, rendered, target, c, width, height);
+        for (size_t i = 0; i < np; ++i) { /* loss.cpp:210-216 */
+            double da, db, dd;
+            ssim_acc += loss_ssim_terms(p.mu_x[i], p.mu_y[i], p.sxx[i], p.syy[i], p.sxy[i], &da, &db, &dd);
+            p.fa[i] = scale * da;
+            p.fb[i] = scale * db;
+            p.fd[i] = scale * dd;
+        }
+        if (lambda == 0.0 || !grad) continue;
+        loss_scatter2d(p.fa, p.sa, p.tmp, width, height);
+        loss_scatter2d(p.fb, p.sb, p.tmp, width, height);
+        loss_scatter2d(p.fd, p.sd, p.tmp, width, height);
+        for (size_t i = 0; i < np; ++i) /* loss.cpp:222-224 */
+            grad[i * 3 + c] += p.sa[i] + 2.0 * p.x[i] * p.sb[i] + p.y[i] * p.sd[i];
+    }
+    free(p.block);
+    double mean_ssim = ssim_acc / (double)n;
+    out[1] = l1;
+    out[2] = 0.5 * (1.0 - mean_ssim);
+    out[0] = (1.0 - lambda) * out[1] + lambda * out[2];
+    return DARBS_CPU_OK;
+}
+
 /* ------------------------------------------------------------- parallel_for */
 
 /* parallel_for parallel.hpp:19-33: `threads` workers, static round-robin

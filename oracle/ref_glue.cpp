@@ -2,7 +2,7 @@
 //
 // TEST INFRASTRUCTURE, NOT PRODUCT.  oracle/Makefile compiles this file together
 // with the reference's own, unmodified sources
-//   /root/reference/proj/core/src/{kernel,geometry,rasterizer}.cpp
+//   /root/reference/proj/core/src/{kernel,geometry,rasterizer,loss}.cpp
 // (read where they lie; never copied) against oracle/eigen_shim into
 // oracle/_ref/libdarbs_ref.so.  It only marshals flat FP64 arrays into the
 // reference's types and back; no algorithm of the hot path is restated here
@@ -19,6 +19,7 @@
 #include "darbs/fit_common.hpp"
 #include "darbs/geometry.hpp"
 #include "darbs/kernel.hpp"
+#include "darbs/loss.hpp"
 #include "darbs/optim.hpp"
 #include "darbs/psi_table.hpp"
 #include "darbs/rasterizer.hpp"
@@ -416,6 +417,42 @@ void darbs_cpu_param_grads(double psi, int m, const int32_t* owner, const double
         g[10] += gi[3] * opacity[k] * (1.0 - opacity[k]);
         for (int c = 0; c < 3; ++c) g[11 + c] += gi[c] * rgb[3 * k + c] * (1.0 - rgb[3 * k + c]);
     }
+}
+
+void darbs_cpu_random_image(int width, int height, uint64_t seed, int round_f32, double* rgb) {
+    std::mt19937_64 rng(seed);  // tests/test_loss.cpp:13-19
+    std::uniform_real_distribution<double> u(0.0, 1.0);
+    std::size_t n = std::size_t(width) * height * 3;
+    for (std::size_t i = 0; i < n; ++i) rgb[i] = rf(u(rng), round_f32);
+}
+
+static ImageBuffer to_image(int width, int height, const double* rgb) {
+    ImageBuffer img(width, height);
+    std::memcpy(img.rgb.data(), rgb, sizeof(double) * img.rgb.size());
+    return img;
+}
+
+int darbs_cpu_loss_total(int width, int height, const double* rendered, const double* target,
+                         double lambda, double out[3], double* grad) {
+    try {
+        LossResult r = loss_total(to_image(width, height, rendered), to_image(width, height, target), lambda);
+        out[0] = r.total;
+        out[1] = r.l1;
+        out[2] = r.dssim;
+        if (grad) std::memcpy(grad, r.grad.rgb.data(), sizeof(double) * r.grad.rgb.size());
+    } catch (...) {
+        return status_of_current_exception();
+    }
+    return DARBS_CPU_OK;
+}
+
+int darbs_cpu_ssim(int width, int height, const double* a, const double* b, double* out) {
+    try {
+        *out = ssim(to_image(width, height, a), to_image(width, height, b));
+    } catch (...) {
+        return status_of_current_exception();
+    }
+    return DARBS_CPU_OK;
 }
 
 int darbs_cpu_adam_step(int64_t dim, double* params, const double* grads, double* m, double* v,

@@ -100,6 +100,7 @@ def _load():
     lib.darbs_cuda_prefetch_target.argtypes = [vp, vp, i64]
     lib.darbs_cuda_microbench.argtypes = [vp, C.POINTER(dbl)]
     lib.darbs_cuda_adam_step.argtypes = [vp, i64, vp, vp, vp, vp, vp, i32, i32]
+    lib.darbs_cuda_loss_total.argtypes = [vp, i32, i32, vp, vp, dbl, C.POINTER(dbl), vp, i32]
     lib.darbs_cuda_set_stage_timing.argtypes = [vp, i32]
     lib.darbs_cuda_stage_times.argtypes = [vp, C.POINTER(dbl)]
     lib.darbs_cuda_work_counters.argtypes = [vp, C.POINTER(i64)]
@@ -114,7 +115,7 @@ EXPORTED_SYMBOLS = (
     "darbs_cuda_kernel_preset darbs_cuda_default_psi darbs_cuda_eval darbs_cuda_bin darbs_cuda_forward "
     "darbs_cuda_backward darbs_cuda_realize darbs_cuda_project darbs_cuda_backward_projection "
     "darbs_cuda_evaluate_view darbs_cuda_prefetch_target darbs_cuda_pop_loss darbs_cuda_adam_step darbs_cuda_set_stage_timing darbs_cuda_stage_times "
-    "darbs_cuda_work_counters darbs_cuda_microbench"
+    "darbs_cuda_work_counters darbs_cuda_microbench darbs_cuda_loss_total"
 ).split()
 
 
@@ -285,7 +286,7 @@ class Context:
         out = (C.c_double * 8)()
         self._check(_lib.darbs_cuda_microbench(self._h, out))
         return dict(ffma_per_s=float(out[0]), mufu_per_s=float(out[1]), sm_mhz=float(out[2]), sms=int(out[3]),
-                    ffma_imm_per_s=float(out[4]))
+                    ffma_imm_per_s=float(out[4]), ffma2_per_s=float(out[5]))
 
     def work_counters(self) -> dict:
         out = (C.c_int64 * 8)()
@@ -445,6 +446,16 @@ class Context:
         loss = (C.c_double * 4)()
         self._check(_lib.darbs_cuda_pop_loss(self._h, loss))
         return tuple(float(x) for x in loss)
+
+    def loss_total(self, rendered, target, lam: float, want_grad: bool = True):
+        """loss_total, src/loss.cpp:173-230.  Images are (h, w, 3).  Returns ((total, l1, dssim, mse), grad)."""
+        a = _Args()
+        h, w = int(rendered.shape[0]), int(rendered.shape[1])
+        pr, pt = a.ptr(rendered, np.float32, 3 * w * h), a.ptr(target, np.float32, 3 * w * h)
+        grad, pg = a.out(rendered, (h, w, 3), np.float32) if want_grad else (None, None)
+        loss = (C.c_double * 4)()
+        self._check(_lib.darbs_cuda_loss_total(self._h, w, h, pr, pt, float(lam), loss, pg, a.space))
+        return tuple(float(x) for x in loss), grad
 
     def adam_step(self, params, grads, m, v, lrs, t: int):
         """adam_step, include/darbs/optim.hpp:24-39 (in place)."""

@@ -360,7 +360,7 @@ void darbs_cuda_destroy(darbs_cuda_ctx* ctx) {
     DeviceBuffer* bufs[] = {&ctx->recs, &ctx->rects, &ctx->depth_keys, &ctx->order, &ctx->offsets,
                             &ctx->tile_keys, &ctx->tile_vals, &ctx->ranges, &ctx->streams, &ctx->stream_count, &ctx->cub_temp,
                             &ctx->counters, &ctx->t_final, &ctx->processed, &ctx->contributors,
-                            &ctx->image, &ctx->valid, &ctx->splat_grads, &ctx->grad_image};
+                            &ctx->image, &ctx->valid, &ctx->splat_grads, &ctx->grad_image, &ctx->loss_maps};
     for (DeviceBuffer* b : bufs)
         if (b->ptr) cudaFree(b->ptr);
     for (int i = 0; i < 8; ++i) {
@@ -699,8 +699,8 @@ darbs_status darbs_cuda_evaluate_view(darbs_cuda_ctx* ctx, const darbs_kernel_sp
     if (!camera || !background) return fail(ctx, DARBS_INVALID_PARAMETER, "camera/background is NULL");
     if ((target != nullptr) == (grad_image != nullptr))
         return fail(ctx, DARBS_INVALID_PARAMETER, "pass exactly one of target / grad_image");
-    if (target && lambda != 0.0)
-        return fail(ctx, DARBS_INVALID_PARAMETER, "only lambda == 0 (L1) is implemented in this round");
+    if (target && !(lambda >= 0.0 && lambda <= 1.0))
+        return fail(ctx, DARBS_INVALID_PARAMETER, "lambda must lie in [0, 1]");
     if (n <= 0 || !raw_params) return fail(ctx, DARBS_INVALID_PARAMETER, "empty primitive set");
     if (!(psi > 0.0)) return fail(ctx, DARBS_INVALID_PARAMETER, "apply_psi: psi must be positive");
     DeviceGuard guard(ctx->device);
@@ -762,8 +762,8 @@ darbs_status darbs_cuda_evaluate_view(darbs_cuda_ctx* ctx, const darbs_kernel_sp
     if (target) {
         StageScope ts(ctx, ST_LOSS);
         DARBS_TRY(reserve(ctx, ctx->grad_image, sizeof(float) * 3 * px));
-        DARBS_TRY(launch_l1_loss(ctx, (int64_t)(3 * px), d_image, d_target, lambda,
-                                 (float*)ctx->grad_image.ptr, d_sums));
+        DARBS_TRY(launch_loss(ctx, width, height, d_image, d_target, lambda, (float*)ctx->grad_image.ptr,
+                              d_sums));
         d_gimg = (const float*)ctx->grad_image.ptr;
     }
     if (param_grads) {
@@ -780,7 +780,7 @@ darbs_status darbs_cuda_evaluate_view(darbs_cuda_ctx* ctx, const darbs_kernel_sp
     }
     DARBS_TRY(st.finish());
     DARBS_TRY(sti.finish());
-    // flags (2 ints) and loss sums (2 doubles) travel to a pinned ring slot; the caller either waits
+    // flags (2 ints) and loss sums (3 doubles) travel to a pinned ring slot; the caller either waits
     // for them now (loss_out) or collects them later with darbs_cuda_pop_loss, so that a training
     // loop never has to drain the stream between two iterations
     if (ctx->loss_pending == kLossRing) {  // nobody collects them: forget the oldest
@@ -790,7 +790,7 @@ darbs_status darbs_cuda_evaluate_view(darbs_cuda_ctx* ctx, const darbs_kernel_sp
     LossSlot& slot = ctx->loss_ring[(ctx->loss_head + ctx->loss_pending) % kLossRing];
     slot.count = target ? (double)(3 * px) : 0.0;
     slot.lambda = lambda;
-    DARBS_CUDA_TRY(ctx, cudaMemcpyAsync(slot.host, d_flags, 32, cudaMemcpyDeviceToHost, ctx->stream));
+    DARBS_CUDA_TRY(ctx, cudaMemcpyAsync(slot.host, d_flags, 40, cudaMemcpyDeviceToHost, ctx->stream));
     DARBS_CUDA_TRY(ctx, cudaEventRecord(slot.done, ctx->stream));
     ++ctx->loss_pending;
     if (loss_out) {
@@ -837,10 +837,10 @@ darbs_status darbs_cuda_pop_loss(darbs_cuda_ctx* ctx, double loss_out[4]) {
     const double* sums = (const double*)((const char*)slot.host + 16);
     double out[4] = {0.0, 0.0, 0.0, 0.0};
     if (slot.count > 0.0) {
-        out[1] = sums[0] / slot.count;              // l1      loss.cpp:188
-        out[2] = 0.0;                               // dssim (lambda == 0: not evaluated)
-        out[0] = (1.0 - slot.lambda) * out[1];      // total   loss.cpp:228
-        out[3] = sums[1] / slot.count;              // mse     image.cpp mse()
+        out[1] = sums[0] / slot.count;                                   // l1      loss.cpp:188
+        out[2] = 0.5 * sums[2] / slot.count;                             // dssim   loss.cpp:226-227 (sum of 1 - SSIM)
+        out[0] = (1.0 - slot.lambda) * out[1] + slot.lambda * out[2];    // total   loss.cpp:228
+        out[3] = sums[1] / slot.count;                                   // mse     image.cpp mse()
     }
     if (loss_out)
         for (int i = 0; i < 4; ++i) loss_out[i] = out[i];
@@ -848,6 +848,42 @@ darbs_status darbs_cuda_pop_loss(darbs_cuda_ctx* ctx, double loss_out[4]) {
     if (flags[0] & 2) return fail(ctx, DARBS_NUMERIC_ERROR, "conic_and_radius: covariance not positive definite");
     if (flags[1] == 0) return fail(ctx, DARBS_NUMERIC_ERROR, "fit_scene: all primitives culled in one view");
     if (slot.count > 0.0 && !std::isfinite(out[0])) return fail(ctx, DARBS_NUMERIC_ERROR, "fit_scene: loss diverged");
+    return DARBS_OK;
+}
+
+darbs_status darbs_cuda_loss_total(darbs_cuda_ctx* ctx, int width, int height, const float* rendered,
+                                   const float* target, double lambda, double loss_out[4],
+                                   float* grad_image, darbs_space space) {
+    CTX_OR_FAIL(ctx);
+    if (width < 0 || height < 0) return fail(ctx, DARBS_INVALID_PARAMETER, "loss_total: negative size");
+    const size_t px = (size_t)width * height;
+    if (px > 0 && (!rendered || !target)) return fail(ctx, DARBS_INVALID_PARAMETER, "loss_total: image is NULL");
+    if (!(lambda >= 0.0 && lambda <= 1.0)) return fail(ctx, DARBS_INVALID_PARAMETER, "lambda must lie in [0, 1]");
+    DeviceGuard guard(ctx->device);
+    reset_stage_marks(ctx, {ST_LOSS});
+    Stager st(ctx, space);
+    const float *d_img, *d_tgt;
+    float* d_grad;
+    DARBS_TRY(st.in(rendered, 3 * px, &d_img));
+    DARBS_TRY(st.in(target, 3 * px, &d_tgt));
+    DARBS_TRY(st.out(grad_image, 3 * px, &d_grad));
+    double* d_sums = (double*)((unsigned long long*)ctx->counters.ptr + 14);
+    {
+        StageScope ts(ctx, ST_LOSS);
+        DARBS_TRY(launch_loss(ctx, width, height, d_img, d_tgt, lambda, d_grad, d_sums));
+    }
+    DARBS_TRY(st.finish());
+    if (loss_out) {
+        DARBS_CUDA_TRY(ctx, cudaMemcpyAsync(ctx->pinned, d_sums, sizeof(double) * 3, cudaMemcpyDeviceToHost,
+                                            ctx->stream));
+        DARBS_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+        const double* sums = (const double*)ctx->pinned;
+        const double count = (double)(3 * px);
+        loss_out[1] = px ? sums[0] / count : 0.0;                      // loss.cpp:188
+        loss_out[2] = px ? 0.5 * sums[2] / count : 0.0;                // loss.cpp:226-227 (sum of 1 - SSIM)
+        loss_out[0] = (1.0 - lambda) * loss_out[1] + lambda * loss_out[2];
+        loss_out[3] = px ? sums[1] / count : 0.0;
+    }
     return DARBS_OK;
 }
 

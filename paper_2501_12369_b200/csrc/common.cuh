@@ -105,6 +105,7 @@ struct darbs_cuda_ctx {
     darbs_b200::DeviceBuffer valid;        // per-primitive visibility (evaluate_view)
     darbs_b200::DeviceBuffer splat_grads;  // 12n: SplatGrads rows padded to 12 floats
     darbs_b200::DeviceBuffer grad_image;   // 3wh
+    darbs_b200::DeviceBuffer loss_maps;    // 9wh: the three SSIM partial maps (loss.cu)
     void* pinned = nullptr;                // small pinned host scratch
     size_t pinned_bytes = 0;
 
@@ -209,5 +210,10 @@ darbs_status launch_adam(darbs_cuda_ctx* ctx, int64_t dim, float* params, const 
 darbs_status launch_l1_loss(darbs_cuda_ctx* ctx, int64_t count, const float* image,
                             const float* target, double lambda, float* grad_image,
                             double* sums /* device: abs sum, sq sum */);
+
+// loss.cu
+darbs_status launch_loss(darbs_cuda_ctx* ctx, int width, int height, const float* image,
+                         const float* target, double lambda, float* grad_image,
+                         double* sums /* device, 5 doubles: abs sum, sq sum, sum of (1 - SSIM), 2 scratch */);
 
 }  // namespace darbs_b200

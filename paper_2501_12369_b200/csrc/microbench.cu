@@ -40,6 +40,32 @@ __global__ void __launch_bounds__(1024) ffma_kernel(float seed, float* sink, lon
     if (blockIdx.x == 0 && threadIdx.x == 0) cycles[0] = t1 - t0;
 }
 
+// Packed FP32 FMA (fma.rn.f32x2, FFMA2 in SASS): two FMAs per lane per instruction.
+__global__ void __launch_bounds__(1024) ffma2_kernel(float seed, float* sink) {
+    float2 a0 = make_float2(seed + threadIdx.x, seed + 0.5f), a1 = a0, a2 = a0, a3 = a0, a4 = a0, a5 = a0, a6 = a0,
+           a7 = a0;
+    a1.x += 1.f; a2.x += 2.f; a3.x += 3.f; a4.x += 4.f; a5.x += 5.f; a6.x += 6.f; a7.x += 7.f;
+    const float mm = 0.999f + (float)(blockIdx.x >> 30), cc = 0.001f + (float)(blockIdx.x >> 29);
+    const float2 m = make_float2(mm, mm), c = make_float2(cc, cc);
+#pragma unroll 1
+    for (int i = 0; i < kIters; ++i) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            a0 = __ffma2_rn(a0, m, c);
+            a1 = __ffma2_rn(a1, m, c);
+            a2 = __ffma2_rn(a2, m, c);
+            a3 = __ffma2_rn(a3, m, c);
+            a4 = __ffma2_rn(a4, m, c);
+            a5 = __ffma2_rn(a5, m, c);
+            a6 = __ffma2_rn(a6, m, c);
+            a7 = __ffma2_rn(a7, m, c);
+        }
+    }
+    float s = a0.x + a1.x + a2.x + a3.x + a4.x + a5.x + a6.x + a7.x + a0.y + a1.y + a2.y + a3.y + a4.y + a5.y +
+              a6.y + a7.y;
+    if (s == 12345.678f) sink[0] = s;
+}
+
 __global__ void __launch_bounds__(1024) mufu_kernel(float seed, float* sink) {
     float a0 = seed + 1e-3f * threadIdx.x, a1 = a0 - 0.1f, a2 = a0 - 0.2f, a3 = a0 - 0.3f;
 #pragma unroll 1
@@ -73,7 +99,14 @@ extern "C" darbs_status darbs_cuda_microbench(darbs_cuda_ctx* ctx, double out[8]
     float* sink = (float*)((unsigned long long*)ctx->counters.ptr + 20);
     long long* cycles = (long long*)((unsigned long long*)ctx->counters.ptr + 22);
     cudaEvent_t e0 = ctx->timer.ev[14], e1 = ctx->timer.ev[15];
-    float ms_f = 0.f, ms_m = 0.f, ms_i = 0.f;
+    float ms_f = 0.f, ms_m = 0.f, ms_i = 0.f, ms_2 = 0.f;
+    for (int rep = 0; rep < 3; ++rep) {
+        DARBS_CUDA_TRY(ctx, cudaEventRecord(e0, ctx->stream));
+        ffma2_kernel<<<blocks, threads, 0, ctx->stream>>>(1.0f, sink);
+        DARBS_CUDA_TRY(ctx, cudaEventRecord(e1, ctx->stream));
+        DARBS_CUDA_TRY(ctx, cudaEventSynchronize(e1));
+        DARBS_CUDA_TRY(ctx, cudaEventElapsedTime(&ms_2, e0, e1));
+    }
     for (int rep = 0; rep < 3; ++rep) {
         DARBS_CUDA_TRY(ctx, cudaEventRecord(e0, ctx->stream));
         ffma_kernel<true><<<blocks, threads, 0, ctx->stream>>>(1.0f, sink, cycles);
@@ -95,7 +128,7 @@ extern "C" darbs_status darbs_cuda_microbench(darbs_cuda_ctx* ctx, double out[8]
         DARBS_CUDA_TRY(ctx, cudaEventSynchronize(e1));
         DARBS_CUDA_TRY(ctx, cudaEventElapsedTime(&ms_m, e0, e1));
     }
-    DARBS_TRY(check_launch(ctx, "microbench", 9));
+    DARBS_TRY(check_launch(ctx, "microbench", 12));
     long long cyc = 0;
     DARBS_CUDA_TRY(ctx, cudaMemcpy(&cyc, cycles, sizeof(cyc), cudaMemcpyDeviceToHost));
     const double n_thr = (double)blocks * threads;
@@ -106,7 +139,8 @@ extern "C" darbs_status darbs_cuda_microbench(darbs_cuda_ctx* ctx, double out[8]
     out[2] = (double)cyc / (ms_f * 1e-3) / 1e6;
     out[3] = (double)sms;
     out[4] = n_thr * kIters * 32.0 / (ms_i * 1e-3);
-    out[5] = out[6] = out[7] = 0.0;
+    out[5] = n_thr * kIters * 32.0 / (ms_2 * 1e-3);  // packed instructions per second (x4 = FLOP/s)
+    out[6] = out[7] = 0.0;
     if (prev >= 0 && prev != ctx->device) cudaSetDevice(prev);
     return DARBS_OK;
 }

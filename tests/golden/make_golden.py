@@ -4,7 +4,7 @@
 The reference (arxiv/paper_2501_12369, proj/core) ships no golden images: every known answer in
 its tests is closed-form or "reference vs its own brute-force oracle".  These
 fixtures are therefore outputs of the reference itself: oracle/_ref/libdarbs_ref.so is
-/root/reference/proj/core/src/{kernel,geometry,rasterizer}.cpp compiled unmodified against
+/root/reference/proj/core/src/{kernel,geometry,rasterizer,loss}.cpp compiled unmodified against
 oracle/eigen_shim (oracle/Makefile `ref`).  /root/reference does not exist on the GPU box, so the
 vectors are committed; this script is how they were made:
 
@@ -126,6 +126,37 @@ def adam_case(ref):
     return out
 
 
+def smooth_image(w, h, seed):
+    """A renderer-like image: a few soft blobs on a gradient, float32-representable, in [0, 1]."""
+    rng = np.random.default_rng(seed)
+    yy, xx = np.mgrid[0:h, 0:w]
+    img = np.zeros((h, w, 3))
+    for _ in range(6):
+        cx, cy, s = rng.uniform(0, w), rng.uniform(0, h), rng.uniform(2.0, 0.4 * max(w, h))
+        img += np.exp(-((xx - cx) ** 2 + (yy - cy) ** 2) / (2 * s * s))[..., None] * rng.uniform(0, 0.6, 3)
+    img += 0.2 * (xx / max(w - 1, 1))[..., None]
+    return f32r(np.clip(img, 0.0, 1.0))
+
+
+def loss_case(ref):
+    """loss_total (loss.cpp:173-230) on the test fixture's random images (tests/test_loss.cpp:13-19)
+    and on a smooth pair, at sizes that exercise single and repeated mirror reflection."""
+    out = {}
+    for tag, (w, h) in {"a": (10, 9), "b": (37, 21), "c": (3, 4), "d": (70, 45)}.items():
+        x = ref.random_image(w, h, 3)
+        y = ref.random_image(w, h, 4)
+        if tag == "d":
+            x = smooth_image(w, h, 5)
+            y = f32r(np.clip(x + np.random.default_rng(6).normal(scale=0.02, size=x.shape), 0, 1))
+        out[tag + "/rendered"], out[tag + "/target"] = x.astype(np.float32), y.astype(np.float32)
+        for lam in (0.0, 0.2, 1.0):
+            st, vals, grad = ref.loss_total(x, y, lam)
+            assert st == 0
+            out[f"{tag}/{lam}/values"] = np.array(vals)
+            out[f"{tag}/{lam}/grad"] = grad
+    return out
+
+
 def main():
     if not cpu.available("reference"):
         raise SystemExit("oracle/_ref/libdarbs_ref.so missing: run `make -C oracle ref` where /root/reference exists")
@@ -138,6 +169,7 @@ def main():
         np.savez_compressed(os.path.join(HERE, f"geometry_{name}.npz"), **geometry_case(ref, name, 120, 9))
     np.savez_compressed(os.path.join(HERE, "eval.npz"), **eval_case(ref))
     np.savez_compressed(os.path.join(HERE, "adam.npz"), **adam_case(ref))
+    np.savez_compressed(os.path.join(HERE, "loss.npz"), **loss_case(ref))
     total = sum(os.path.getsize(os.path.join(HERE, f)) for f in os.listdir(HERE) if f.endswith(".npz"))
     print(f"wrote golden fixtures, {total / 1024:.0f} KiB")
 

@@ -39,7 +39,7 @@ def test_library_exports_every_declared_symbol(darbs):
 def test_every_entry_point_cites_the_reference():
     """Each declaration is preceded by a comment naming the reference interface it replaces."""
     text = open(HEADER).read()
-    for name in ("forward", "backward", "bin", "project", "backward_projection", "evaluate_view", "adam_step",
+    for name in ("forward", "backward", "bin", "project", "backward_projection", "evaluate_view", "adam_step", "loss_total",
                  "make_kernel", "kernel_preset", "eval", "realize"):
         i = text.index(f"darbs_cuda_{name}(")
         assert re.search(r"\b(src|include)/[\w/]+\.(cpp|hpp):\d+", text[max(0, i - 1500):i]), name

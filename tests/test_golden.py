@@ -112,6 +112,20 @@ def test_port_reproduces_eval_and_adam_golden(port):
         assert np.abs(m - z[f"m{t}"]).max() <= 1e-15 and np.abs(v - z[f"v{t}"]).max() <= 1e-15
 
 
+LOSS_TAGS = ("a", "b", "c", "d")
+
+
+def test_port_reproduces_loss_golden(port):
+    z = np.load(os.path.join(GOLD, "loss.npz"))
+    for tag in LOSS_TAGS:
+        x, y = z[tag + "/rendered"].astype(np.float64), z[tag + "/target"].astype(np.float64)
+        for lam in (0.0, 0.2, 1.0):
+            st, vals, grad = port.loss_total(x, y, lam)
+            assert st == 0
+            assert np.abs(np.array(vals) - z[f"{tag}/{lam}/values"]).max() <= 1e-13
+            assert np.abs(grad - z[f"{tag}/{lam}/grad"]).max() <= 1e-15
+
+
 # ----------------------------------------------------------------------------- GPU: the C ABI
 @pytest.mark.gpu
 @pytest.mark.parametrize("path", RASTER, ids=ident)
@@ -180,3 +194,19 @@ def test_gpu_reproduces_eval_and_adam_golden(ctx, darbs):
     for t in (1, 2, 3):
         ctx.adam_step(p, f32(z["grads"]), m, v, f32(z["lrs"]), t)
         assert np.abs(p - z[f"params{t}"]).max() <= 1e-6
+
+
+@pytest.mark.gpu
+def test_gpu_reproduces_loss_golden(ctx):
+    """loss_total through the C ABI against the reference's own outputs.  Tolerances: values 2e-6
+    absolute (FP32 moments, FP64 sums); gradient max |g - g_ref| <= 1e-5 max |g_ref| and
+    |g - g_ref| <= 1e-3 max(|g|, |g_ref|, floor) with floor = 1e-2 of the largest reference gradient."""
+    z = np.load(os.path.join(GOLD, "loss.npz"))
+    for tag in LOSS_TAGS:
+        x, y = z[tag + "/rendered"], z[tag + "/target"]
+        for lam in (0.0, 0.2, 1.0):
+            vals, grad = ctx.loss_total(x, y, lam)
+            ref_vals, ref_grad = z[f"{tag}/{lam}/values"], z[f"{tag}/{lam}/grad"]
+            assert np.abs(np.array(vals[:3]) - ref_vals).max() <= 2e-6
+            assert np.abs(grad - ref_grad).max() <= 1e-5 * np.abs(ref_grad).max()
+            assert rel_err(grad, ref_grad, 1e-2 * np.abs(ref_grad).max()).max() <= 1e-3

@@ -223,8 +223,31 @@ def test_evaluate_view_l1_loss_and_errors(ctx, port, darbs):
         ctx.evaluate_view(gk, 1.0, raw_behind, DEMO_CAMERA, (0, 0, 0), target=target, param_grads=pg)
     assert e.value.status == 2
     with pytest.raises(darbs.DarbsError) as e:
-        ctx.evaluate_view(gk, 1.0, raw, DEMO_CAMERA, (0, 0, 0), target=target, lam=0.2, param_grads=pg)
+        ctx.evaluate_view(gk, 1.0, raw, DEMO_CAMERA, (0, 0, 0), target=target, lam=1.5, param_grads=pg)
     assert e.value.status == 1
+
+
+@pytest.mark.parametrize("lam", [0.2, 1.0])
+def test_evaluate_view_dssim_loss(ctx, port, darbs, lam):
+    """The full loss_total of fit_scene (loss.cpp:173-230, lambda = 0.2 by default,
+    fit_common.hpp:16) inside evaluate_view: reported values against the oracle's loss on the
+    rendered image, parameter gradients against the same view driven by the oracle's dL/dimage."""
+    gk = darbs.kernel_preset("half-cosine-sq")
+    psi = darbs.default_psi("half-cosine-sq")
+    n, w, h = 300, 64, 64
+    raw = random_raw(n, 5)
+    img = np.zeros((h, w, 3), np.float32)
+    ctx.evaluate_view(gk, psi, raw, DEMO_CAMERA, (0, 0, 0), grad_image=np.zeros((h, w, 3), np.float32),
+                      image_out=img)
+    target = np.clip(img + f32(np.random.default_rng(1).normal(scale=0.05, size=img.shape)), 0, 1)
+    pg = np.zeros((n, 14), np.float32)
+    total, l1, dssim, mse = ctx.evaluate_view(gk, psi, raw, DEMO_CAMERA, (0, 0, 0), target=target, lam=lam,
+                                              param_grads=pg)
+    st, (r_total, r_l1, r_dssim), r_grad = port.loss_total(img.astype(np.float64), target.astype(np.float64), lam)
+    assert (total, l1, dssim) == pytest.approx((r_total, r_l1, r_dssim), abs=2e-6)
+    pg_ref = np.zeros((n, 14), np.float32)
+    ctx.evaluate_view(gk, psi, raw, DEMO_CAMERA, (0, 0, 0), grad_image=f32(r_grad), param_grads=pg_ref)
+    assert rel_err(pg, pg_ref, 1e-3 * np.abs(pg_ref).max()).max() <= 2e-3
 
 
 def test_adam_matches_oracle(ctx, port):

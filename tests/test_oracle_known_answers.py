@@ -408,6 +408,72 @@ def test_adam_known_answers(any_oracle):
 
 
 # ------------------------------------------------------------------ restatement == reference
+# ------------------------------------------------------------------ loss (tests/test_loss.cpp:23-82)
+def test_loss_identical_images(any_oracle):
+    """test_loss.cpp:23-34"""
+    o = any_oracle
+    x = o.random_image(16, 16, 1, round_f32=False)
+    st, s = o.ssim(x, x)
+    assert st == 0 and s == pytest.approx(1.0, rel=1e-12)
+    for lam in (0.0, 0.2, 1.0):
+        st, (total, l1, dssim), grad = o.loss_total(x, x, lam)
+        assert st == 0
+        assert abs(total) <= 1e-12 and l1 == 0.0 and abs(dssim) <= 1e-12
+        assert np.abs(grad).max() < 1e-12
+
+
+def test_loss_pure_l1_on_constant_offset(any_oracle):
+    """test_loss.cpp:36-45"""
+    o = any_oracle
+    x = np.minimum(o.random_image(12, 12, 2, round_f32=False), 0.8)
+    st, (total, l1, dssim), _ = o.loss_total(x + 0.1, x, 0.0)
+    assert total == pytest.approx(0.1, rel=1e-12) and l1 == pytest.approx(0.1, rel=1e-12)
+
+
+def test_loss_gradient_matches_finite_differences(any_oracle):
+    """test_loss.cpp:53-77: central differences, step 1e-6, every 7th value, rel < 1e-3."""
+    o = any_oracle
+    w, h = 10, 9
+    x = o.random_image(w, h, 3, round_f32=False)
+    y = o.random_image(w, h, 4, round_f32=False)
+    for lam in (0.2, 1.0):
+        st, _, grad = o.loss_total(x, y, lam)
+        worst = 0.0
+        flat = grad.reshape(-1)
+        for i in range(0, x.size, 7):
+            hi, lo = x.copy().reshape(-1), x.copy().reshape(-1)
+            hi[i] += 1e-6
+            lo[i] -= 1e-6
+            fd = (o.loss_total(hi.reshape(x.shape), y, lam, want_grad=False)[1][0] -
+                  o.loss_total(lo.reshape(x.shape), y, lam, want_grad=False)[1][0]) / 2e-6
+            worst = max(worst, abs(fd - flat[i]) / max(abs(fd), abs(flat[i]), 1e-8))
+        assert worst < 1e-3
+
+
+def test_loss_mixes_linearly_in_lambda(any_oracle):
+    """test_loss.cpp:79-86"""
+    o = any_oracle
+    x = o.random_image(14, 14, 5, round_f32=False)
+    y = o.random_image(14, 14, 6, round_f32=False)
+    l0 = o.loss_total(x, y, 0.0)[1]
+    l1 = o.loss_total(x, y, 1.0)[1]
+    mid = o.loss_total(x, y, 0.3)[1]
+    assert mid[0] == pytest.approx(0.7 * l0[1] + 0.3 * l1[2], rel=1e-12)
+
+
+@pytest.mark.parametrize("size", [(1, 1), (3, 4), (10, 9), (37, 21), (64, 48)])
+def test_port_loss_matches_reference_sources(port, ref, size):
+    w, h = size
+    x, y = port.random_image(w, h, 11), port.random_image(w, h, 12)
+    assert np.array_equal(x, ref.random_image(w, h, 11))
+    for lam in (0.0, 0.2, 1.0):
+        _, a, ga = port.loss_total(x, y, lam)
+        _, b, gb = ref.loss_total(x, y, lam)
+        # (1x1: every tap folds onto the one pixel, b2 = C2 exactly up to rounding -> 1e-14 noise)
+        assert np.abs(np.array(a) - np.array(b)).max() <= 1e-12
+        assert np.abs(ga - gb).max() <= 1e-12 * max(1.0, np.abs(gb).max())
+
+
 @pytest.mark.parametrize("name", PRESETS)
 def test_port_matches_reference_sources(port, ref, name):
     """The plain-C restatement against the reference's own sources on the same inputs: integer
