@@ -4,7 +4,7 @@
 Workload (BASELINE.json configs[2], the configuration the metric "train iters/sec (fwd+bwd) at
 1M splats 1080p per DARBF kernel" is quoted on): 1 000 000 synthetic primitives, 1920x1080, one
 camera view per GPU, one full training iteration per DARBF kernel = preprocess -> bin/sort ->
-render forward -> L1 loss -> render backward -> preprocess backward -> Adam
+render forward -> loss (L1 + D-SSIM, lambda 0.2) -> render backward -> preprocess backward -> Adam
 (fit_scene's evaluate + adam_step, src/fit3d.cpp:104-184).  One "step" runs that iteration once
 for each of the four kernels (gaussian, half-cosine-sq, raised-cosine, inv-multiquadratic);
 ``value`` = view-iterations per second over the whole job (4 * steps * n_gpus / seconds), i.e. the
@@ -37,12 +37,13 @@ FP_K = {"gaussian": (1, 0), "half-cosine-sq": (2, 1), "raised-cosine": (4, 2), "
 METRIC = "train_view_iters_per_sec_1M_splats_1080p"
 UNIT = "view-iters/s (fwd+bwd+Adam, mean over the 4 DARBF kernels)"
 SAMPLE_FRACTION = 16
+LAMBDA = 0.2  # FitConfig::lambda, include/darbs/fit_common.hpp:16: L = (1 - lambda) L1 + lambda (1 - SSIM)/2
 
 
 def parse_args():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--splats", type=int, default=1_000_000)
@@ -125,8 +126,7 @@ def cpu_iteration(orc, cpu, name, raw64, cam, target, lrs64, state, threads):
     s = cpu.Scene(pr["mu2"][vis], None, pr["conic"][vis], pr["radius"][vis], pr["depth"][vis], prims[vis, 10],
                   prims[vis, 11:14])
     fr = orc.forward(k, s, w, h, (0.0, 0.0, 0.0), threads=threads, keep=True)
-    d = fr["image"] - target
-    gimg = np.sign(d) / d.size  # loss.cpp:183-188 with lambda = 0
+    st, _vals, gimg = orc.loss_total(fr["image"], target, LAMBDA)  # fit3d.cpp:122
     st, sg = orc.backward(fr["handle"], k, gimg, s, threads=threads)
     orc.forward_free(fr["handle"])
     grads = orc.param_grads(psi, vis, sg, s.conic, s.opacity, s.rgb, prims, cam)
@@ -202,7 +202,8 @@ def run_reference_arm(args):
 def workload_config(args, n_gpus):
     return {
         "workload": f"{args.splats} synthetic 3-D primitives (scene B, SURVEY 8d), {args.width}x{args.height}, "
-                    f"1 orbit view per GPU, full training iteration (preprocess, bin+sort, render fwd, L1 loss, "
+                    f"1 orbit view per GPU, full training iteration (preprocess, bin+sort, render fwd, L1 + D-SSIM loss "
+                    f"with lambda {LAMBDA}, "
                     f"render bwd, preprocess bwd, Adam) for each of {', '.join(KERNELS)}",
         "splats": args.splats, "width": args.width, "height": args.height, "views_per_step": n_gpus,
         "parallelism": f"view-parallel x{n_gpus}, NCCL all-reduce of 14N f32 parameter gradients" if n_gpus > 1
@@ -262,12 +263,12 @@ def run_ours(args):
             # the view's target image comes from pinned host memory through the C ABI
             # (image_space = DARBS_HOST); the loss of every iteration is read back to the host, one
             # iteration late (darbs_cuda_pop_loss) so that the read-back never drains the stream
-            loss = ctx.evaluate_view(k, psi, s["params"], cam, bg, target=s["target_np"], lam=0.0,
+            loss = ctx.evaluate_view(k, psi, s["params"], cam, bg, target=s["target_np"], lam=LAMBDA,
                                      param_grads=s["grads"], want_loss=False)
             # the next iteration's target starts its upload under this iteration's render kernels
             ctx.prefetch_target(state[KERNELS[(KERNELS.index(name) + 1) % len(KERNELS)]]["target_np"])
         else:
-            loss = ctx.evaluate_view(k, psi, s["params"], cam, bg, target=s["target"], lam=0.0,
+            loss = ctx.evaluate_view(k, psi, s["params"], cam, bg, target=s["target"], lam=LAMBDA,
                                      param_grads=s["grads"], want_loss=False)
         if world > 1:
             dist.all_reduce(s["grads"], op=dist.ReduceOp.SUM)  # gradients are summed over views, fit3d.cpp:148-158
@@ -352,7 +353,7 @@ def run_ours(args):
         reps = 3
         for _ in range(reps):
             s["grads"].zero_()
-            ctx.evaluate_view(k, psi, s["params"], cam, bg, target=s["target"], lam=0.0, param_grads=s["grads"])
+            ctx.evaluate_view(k, psi, s["params"], cam, bg, target=s["target"], lam=LAMBDA, param_grads=s["grads"])
             st = ctx.stage_times()
             ctx.adam_step(s["params"].view(-1), s["grads"].view(-1), s["m"], s["v"], lrs, s["t"] + 1)
             st["adam"] = ctx.stage_times()["adam"]
@@ -410,6 +411,7 @@ def run_ours(args):
                        "MEASURED_PEAKS.json has no FP32/MUFU entry",
         "peak_mufu_gops": peaks["mufu_per_s"] / 1e9, "peak_sm_mhz": peaks["sm_mhz"],
         "peak_ffma_imm_tflops": 2.0 * peaks["ffma_imm_per_s"] / 1e12,
+        "peak_ffma2_tflops": 4.0 * peaks["ffma2_per_s"] / 1e12,
         "algorithmic_work": "flops = V*(13+F_k[+F'_k]) + {9|57}*C per launch with V = sum processed, C = sum "
                             "contributors of that launch (SURVEY 8d); frac = max(flops/peak_fp32, mufu/peak_mufu)/t; "
                             "block-level culling skips visits this count includes, so frac can exceed 1 "
@@ -432,6 +434,8 @@ def run_ours(args):
                 "preprocess": (56 + 48) * n / (st["preprocess"] * 1e-3) / 1e9 / hbm_peak,
                 "preprocess_bwd": (36 + 56 + 56) * n / (st["preprocess_bwd"] * 1e-3) / 1e9 / hbm_peak,
                 "adam": 28 * 14 * n / (st["adam"] * 1e-3) / 1e9 / hbm_peak,
+                # loss: image + target read twice, three partial maps written and read, gradient written
+                "loss": (4 * 12 + 2 * 36 + 12) * w * h / (st["loss"] * 1e-3) / 1e9 / hbm_peak,
                 # rect 60 B + depth sort (4 digit passes x 16 B + 4 B histogram read) per splat;
                 # duplicate 8 B + tile sort (2 passes x 16 B + 4 B) + ranges 4 B per tile entry
                 "binning_sort": (128 * n + 48 * kk) / (st["binning"] * 1e-3) / 1e9 / hbm_peak,
