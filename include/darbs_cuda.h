@@ -111,6 +111,20 @@ DARBS_API int64_t darbs_cuda_launch_count(const darbs_cuda_ctx* ctx);
  * in FP64 exactly as the reference takes them (default).  0: pure FP32. */
 DARBS_API darbs_status darbs_cuda_set_exact_decisions(darbs_cuda_ctx* ctx, int enabled);
 
+/* ---- device memory ----------------------------------------------------------
+ * For callers without a CUDA toolchain of their own (the C++ mirror's fit_scene keeps the raw
+ * parameters, Adam state and target images resident on the GPU; the reference keeps its
+ * std::vectors in host memory, so these have no reference analogue).  Pointers returned by
+ * device_alloc are DARBS_DEVICE pointers for every entry point of this header.  upload is
+ * stream-ordered (the host buffer may be reused on return); download synchronises. */
+DARBS_API darbs_status darbs_cuda_device_alloc(darbs_cuda_ctx* ctx, uint64_t bytes, void** out_ptr);
+DARBS_API darbs_status darbs_cuda_device_free(darbs_cuda_ctx* ctx, void* ptr);
+DARBS_API darbs_status darbs_cuda_upload(darbs_cuda_ctx* ctx, void* dst_device, const void* src_host,
+                                         uint64_t bytes);
+DARBS_API darbs_status darbs_cuda_download(darbs_cuda_ctx* ctx, void* dst_host, const void* src_device,
+                                           uint64_t bytes);
+DARBS_API darbs_status darbs_cuda_device_zero(darbs_cuda_ctx* ctx, void* ptr, uint64_t bytes);
+
 /* ---- kernel family ---------------------------------------------------------- */
 
 /* make_kernel, src/kernel.cpp:42-65 (host-side; validates and fills cutoff). */

@@ -116,6 +116,11 @@ class Oracle:
         lib.darbs_cpu_ssim.argtypes = [C.c_int, C.c_int, _dp, _dp, _dp]
         lib.darbs_cpu_random_image.argtypes = [C.c_int, C.c_int, C.c_uint64, C.c_int, _dp]
         lib.darbs_cpu_random_image.restype = None
+        if hasattr(lib, "darbs_cpu_write_scene"):  # file formats: reference build only
+            lib.darbs_cpu_write_scene.argtypes = [C.c_char_p, C.c_int, _dp]
+            lib.darbs_cpu_read_scene.argtypes = [C.c_char_p, C.c_int, _dp]
+            lib.darbs_cpu_write_cameras.argtypes = [C.c_char_p, C.c_int, _dp]
+            lib.darbs_cpu_write_image.argtypes = [C.c_char_p, C.c_int, C.c_int, _dp, C.c_int]
 
     # ------------------------------------------------------------------ kernel
     @property
@@ -297,6 +302,24 @@ class Oracle:
         out = np.zeros(1)
         st = self.lib.darbs_cpu_ssim(w, h, _d(a), _d(b), _d(out))
         return st, float(out[0])
+
+    # ---- file formats (reference build only)
+    def write_scene(self, path, prims):
+        prims = _f64(prims)
+        return self.lib.darbs_cpu_write_scene(os.fsencode(path), prims.shape[0], _d(prims))
+
+    def read_scene(self, path, capacity=4096):
+        out = np.zeros((capacity, 14))
+        n = self.lib.darbs_cpu_read_scene(os.fsencode(path), capacity, _d(out))
+        return n, out[:max(n, 0)]
+
+    def write_cameras(self, path, cams22):
+        cams22 = _f64(cams22).reshape(-1, 22)
+        return self.lib.darbs_cpu_write_cameras(os.fsencode(path), cams22.shape[0], _d(cams22))
+
+    def write_image(self, path, img, ppm=False):
+        img = _f64(img)
+        return self.lib.darbs_cpu_write_image(os.fsencode(path), img.shape[1], img.shape[0], _d(img), int(ppm))
 
     def adam_step(self, params, grads, m, v, lrs, t):
         params, grads, m, v, lrs = (_f64(a).copy() for a in (params, grads, m, v, lrs))

@@ -23,6 +23,7 @@
 #include "darbs/optim.hpp"
 #include "darbs/psi_table.hpp"
 #include "darbs/rasterizer.hpp"
+#include "darbs/scene_io.hpp"
 #include "darbs_cpu.h"
 
 using namespace darbs;
@@ -449,6 +450,63 @@ int darbs_cpu_loss_total(int width, int height, const double* rendered, const do
 int darbs_cpu_ssim(int width, int height, const double* a, const double* b, double* out) {
     try {
         *out = ssim(to_image(width, height, a), to_image(width, height, b));
+    } catch (...) {
+        return status_of_current_exception();
+    }
+    return DARBS_CPU_OK;
+}
+
+// ---- file formats (reference build only): src/scene_io.cpp, src/image.cpp.  Used by
+// tests/golden/make_golden.py to write the I/O fixtures the C++ mirror is byte-compared with.
+int darbs_cpu_write_scene(const char* path, int n, const double* prims) {
+    try {
+        std::vector<Primitive3D> v;
+        for (int i = 0; i < n; ++i) v.push_back(to_prim(prims + 14 * std::size_t(i)));
+        write_scene(v, path);
+    } catch (...) {
+        return status_of_current_exception();
+    }
+    return DARBS_CPU_OK;
+}
+
+int darbs_cpu_read_scene(const char* path, int capacity, double* prims) {
+    try {
+        std::vector<Primitive3D> v = read_scene(path);
+        for (std::size_t i = 0; i < v.size() && int(i) < capacity; ++i) {
+            double* o = prims + 14 * i;
+            for (int k = 0; k < 3; ++k) o[k] = v[i].mu[k];
+            for (int k = 0; k < 3; ++k) o[3 + k] = v[i].scale[k];
+            o[6] = v[i].rot.w();
+            o[7] = v[i].rot.x();
+            o[8] = v[i].rot.y();
+            o[9] = v[i].rot.z();
+            o[10] = v[i].opacity;
+            for (int k = 0; k < 3; ++k) o[11 + k] = v[i].color[k];
+        }
+        return int(v.size());
+    } catch (...) {
+        return -status_of_current_exception();
+    }
+}
+
+int darbs_cpu_write_cameras(const char* path, int n, const double* cams22) {
+    try {
+        std::vector<Camera> v;
+        for (int i = 0; i < n; ++i) v.push_back(to_camera(cams22 + 22 * std::size_t(i)));
+        write_cameras(v, path);
+    } catch (...) {
+        return status_of_current_exception();
+    }
+    return DARBS_CPU_OK;
+}
+
+int darbs_cpu_write_image(const char* path, int width, int height, const double* rgb, int as_ppm) {
+    try {
+        ImageBuffer img = to_image(width, height, rgb);
+        if (as_ppm)
+            write_ppm(img, path);
+        else
+            write_float_dump(img, path);
     } catch (...) {
         return status_of_current_exception();
     }

@@ -101,6 +101,11 @@ def _load():
     lib.darbs_cuda_microbench.argtypes = [vp, C.POINTER(dbl)]
     lib.darbs_cuda_adam_step.argtypes = [vp, i64, vp, vp, vp, vp, vp, i32, i32]
     lib.darbs_cuda_loss_total.argtypes = [vp, i32, i32, vp, vp, dbl, C.POINTER(dbl), vp, i32]
+    lib.darbs_cuda_device_alloc.argtypes = [vp, C.c_uint64, C.POINTER(vp)]
+    lib.darbs_cuda_device_free.argtypes = [vp, vp]
+    lib.darbs_cuda_upload.argtypes = [vp, vp, vp, C.c_uint64]
+    lib.darbs_cuda_download.argtypes = [vp, vp, vp, C.c_uint64]
+    lib.darbs_cuda_device_zero.argtypes = [vp, vp, C.c_uint64]
     lib.darbs_cuda_set_stage_timing.argtypes = [vp, i32]
     lib.darbs_cuda_stage_times.argtypes = [vp, C.POINTER(dbl)]
     lib.darbs_cuda_work_counters.argtypes = [vp, C.POINTER(i64)]
@@ -115,7 +120,8 @@ EXPORTED_SYMBOLS = (
     "darbs_cuda_kernel_preset darbs_cuda_default_psi darbs_cuda_eval darbs_cuda_bin darbs_cuda_forward "
     "darbs_cuda_backward darbs_cuda_realize darbs_cuda_project darbs_cuda_backward_projection "
     "darbs_cuda_evaluate_view darbs_cuda_prefetch_target darbs_cuda_pop_loss darbs_cuda_adam_step darbs_cuda_set_stage_timing darbs_cuda_stage_times "
-    "darbs_cuda_work_counters darbs_cuda_microbench darbs_cuda_loss_total"
+    "darbs_cuda_work_counters darbs_cuda_microbench darbs_cuda_loss_total darbs_cuda_device_alloc "
+    "darbs_cuda_device_free darbs_cuda_upload darbs_cuda_download darbs_cuda_device_zero"
 ).split()
 
 

@@ -413,6 +413,56 @@ darbs_status darbs_cuda_set_exact_decisions(darbs_cuda_ctx* ctx, int enabled) {
     return DARBS_OK;
 }
 
+// ---- device memory ---------------------------------------------------------------
+
+darbs_status darbs_cuda_device_alloc(darbs_cuda_ctx* ctx, uint64_t bytes, void** out_ptr) {
+    CTX_OR_FAIL(ctx);
+    if (!out_ptr) return fail(ctx, DARBS_INVALID_PARAMETER, "device_alloc: out_ptr is NULL");
+    *out_ptr = nullptr;
+    DeviceGuard guard(ctx->device);
+    DARBS_CUDA_TRY(ctx, cudaMalloc(out_ptr, bytes ? (size_t)bytes : 1));
+    return DARBS_OK;
+}
+
+darbs_status darbs_cuda_device_free(darbs_cuda_ctx* ctx, void* ptr) {
+    CTX_OR_FAIL(ctx);
+    if (!ptr) return DARBS_OK;
+    DeviceGuard guard(ctx->device);
+    DARBS_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+    DARBS_CUDA_TRY(ctx, cudaFree(ptr));
+    return DARBS_OK;
+}
+
+darbs_status darbs_cuda_upload(darbs_cuda_ctx* ctx, void* dst_device, const void* src_host, uint64_t bytes) {
+    CTX_OR_FAIL(ctx);
+    if (bytes == 0) return DARBS_OK;
+    if (!dst_device || !src_host) return fail(ctx, DARBS_INVALID_PARAMETER, "upload: NULL pointer");
+    DeviceGuard guard(ctx->device);
+    // pageable source memory is staged by the runtime before the call returns
+    DARBS_CUDA_TRY(ctx, cudaMemcpyAsync(dst_device, src_host, (size_t)bytes, cudaMemcpyHostToDevice, ctx->stream));
+    DARBS_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+    return DARBS_OK;
+}
+
+darbs_status darbs_cuda_download(darbs_cuda_ctx* ctx, void* dst_host, const void* src_device, uint64_t bytes) {
+    CTX_OR_FAIL(ctx);
+    if (bytes == 0) return DARBS_OK;
+    if (!dst_host || !src_device) return fail(ctx, DARBS_INVALID_PARAMETER, "download: NULL pointer");
+    DeviceGuard guard(ctx->device);
+    DARBS_CUDA_TRY(ctx, cudaMemcpyAsync(dst_host, src_device, (size_t)bytes, cudaMemcpyDeviceToHost, ctx->stream));
+    DARBS_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+    return DARBS_OK;
+}
+
+darbs_status darbs_cuda_device_zero(darbs_cuda_ctx* ctx, void* ptr, uint64_t bytes) {
+    CTX_OR_FAIL(ctx);
+    if (bytes == 0) return DARBS_OK;
+    if (!ptr) return fail(ctx, DARBS_INVALID_PARAMETER, "device_zero: NULL pointer");
+    DeviceGuard guard(ctx->device);
+    DARBS_CUDA_TRY(ctx, cudaMemsetAsync(ptr, 0, (size_t)bytes, ctx->stream));
+    return DARBS_OK;
+}
+
 // ---- kernel family ------------------------------------------------------------
 
 darbs_status darbs_cuda_make_kernel(int family, double beta, double xi, int lobes, darbs_kernel_spec* out) {

@@ -26,6 +26,7 @@
 #include <array>
 #include <cstddef>
 #include <cstdint>
+#include <optional>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -130,12 +131,25 @@ inline KernelSpec make_kernel(KernelFamily family, double beta, double xi, int l
     throw_status(darbs_cuda_make_kernel((int)family, beta, xi, lobes, &s), nullptr);
     return from_abi(s);
 }
-inline KernelSpec kernel_preset(const std::string& name) {
+// kernel_preset, kernel.hpp:71 / kernel.cpp:223-240: empty for an unknown name
+inline std::optional<KernelSpec> kernel_preset(const std::string& name) {
     darbs_kernel_spec s;
-    throw_status(darbs_cuda_kernel_preset(name.c_str(), &s), nullptr);
+    if (darbs_cuda_kernel_preset(name.c_str(), &s) != DARBS_OK) return std::nullopt;
     return from_abi(s);
 }
 inline double cutoff_dm2(const KernelSpec& k) { return k.cutoff; }
+inline const char* family_name(KernelFamily f) {  // kernel.cpp:242-256
+    switch (f) {
+        case KernelFamily::Gaussian: return "gaussian";
+        case KernelFamily::HalfCosine: return "half-cosine";
+        case KernelFamily::RaisedCosine: return "raised-cosine";
+        case KernelFamily::ModulusSinc: return "modulus-sinc";
+        default: return "inverse-multiquadratic";
+    }
+}
+struct KernelSample {  // kernel.hpp:34-38
+    double dm2 = 0.0, weight = 0.0, dweight_ddm2 = 0.0;
+};
 
 // ---- geometry / image value types
 struct Conic {
@@ -310,6 +324,16 @@ private:
 inline Session& default_session() {
     thread_local Session s(0);
     return s;
+}
+
+// eval, kernel.hpp:47 / kernel.cpp:127-164, on the device functors (FP64 path of the library)
+inline KernelSample eval(const KernelSpec& spec, double dm2) {
+    darbs_cuda_ctx* ctx = default_session().handle();
+    const darbs_kernel_spec ks = to_abi(spec);
+    const float x = (float)dm2;
+    float w = 0.f, dw = 0.f;
+    throw_status(darbs_cuda_eval(ctx, &ks, 1, &x, &w, &dw, 1, DARBS_HOST), ctx);
+    return KernelSample{dm2, w, dw};
 }
 
 // The reference's free functions (include/darbs/rasterizer.hpp:24-25, :45-46, :65-68).

@@ -34,7 +34,8 @@ static ProjectedSplat iso_splat(Vec2 mu, double s, double depth, double opacity,
 }
 
 int main() {
-    const KernelSpec g = kernel_preset("gaussian");
+    const KernelSpec g = *kernel_preset("gaussian");
+    CHECK(!kernel_preset("no-such-kernel"));
     CHECK(g.unbounded && std::fabs(cutoff_dm2(g) - 9.0) < 1e-12);
     // kernel.cpp:43-51
     bool threw = false;
@@ -90,7 +91,7 @@ int main() {
     {
         std::mt19937_64 rng(3);
         std::uniform_real_distribution<double> u(0.0, 1.0);
-        const KernelSpec k = kernel_preset("half-cosine-sq");
+        const KernelSpec k = *kernel_preset("half-cosine-sq");
         std::vector<ProjectedSplat> splats;
         for (int i = 0; i < 300; ++i)
             splats.push_back(iso_splat(Vec2(64 * u(rng), 48 * u(rng)), 1.0 + 6.0 * u(rng), 0.5 + 9.0 * u(rng),

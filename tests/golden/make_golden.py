@@ -157,6 +157,36 @@ def loss_case(ref):
     return out
 
 
+def io_fixtures(ref):
+    """Files written by the reference's own writers (src/scene_io.cpp, src/image.cpp): the C++ mirror's
+    readers and writers are byte-compared with them (tests/test_host_io.py)."""
+    out = os.path.join(HERE, "io")
+    os.makedirs(out, exist_ok=True)
+    rng = np.random.default_rng(11)
+    n = 12
+    prims = np.zeros((n, 14))
+    prims[:, 0:3] = rng.uniform(-1, 1, (n, 3))
+    prims[:, 3:6] = rng.uniform(0.01, 0.3, (n, 3))
+    prims[:, 6:10] = rng.normal(size=(n, 4))
+    prims[:, 10] = rng.uniform(0, 1, n)
+    prims[:, 11:14] = rng.uniform(0, 1, (n, 3))
+    prims[0, 10], prims[1, 10] = 0.0, 1.0       # the closed ends of the opacity range
+    prims[2, 0:3] = (1e-300, -2.5e17, 1.0 / 3)  # round trips need all 17 digits
+    assert ref.write_scene(os.path.join(out, "scene.txt"), prims) == 0
+    cams = np.stack([DEMO_CAMERA, DEMO_CAMERA])
+    cams[1, 0:6] = (812.5, 799.25, 959.5, 539.5, 1920, 1080)
+    cams[1, 6:22] += rng.normal(scale=1e-3, size=16)
+    assert ref.write_cameras(os.path.join(out, "cameras.txt"), cams) == 0
+    img = rng.uniform(-0.1, 1.1, (7, 9, 3))     # values outside [0, 1] exercise the PPM clamp
+    img[0, 0] = (0.5 / 255.0, 1.5 / 255.0, 254.5 / 255.0)  # rounds half up
+    assert ref.write_image(os.path.join(out, "image.dsfl"), img, ppm=False) == 0
+    assert ref.write_image(os.path.join(out, "image.ppm"), img, ppm=True) == 0
+    # what the PPM of the float dump must be: the dump stores float32, the clamp and rounding see those
+    assert ref.write_image(os.path.join(out, "image_from_dsfl.ppm"), img.astype(np.float32).astype(np.float64),
+                           ppm=True) == 0
+    np.save(os.path.join(out, "scene_values.npy"), prims)
+
+
 def main():
     if not cpu.available("reference"):
         raise SystemExit("oracle/_ref/libdarbs_ref.so missing: run `make -C oracle ref` where /root/reference exists")
@@ -170,6 +200,7 @@ def main():
     np.savez_compressed(os.path.join(HERE, "eval.npz"), **eval_case(ref))
     np.savez_compressed(os.path.join(HERE, "adam.npz"), **adam_case(ref))
     np.savez_compressed(os.path.join(HERE, "loss.npz"), **loss_case(ref))
+    io_fixtures(ref)
     total = sum(os.path.getsize(os.path.join(HERE, f)) for f in os.listdir(HERE) if f.endswith(".npz"))
     print(f"wrote golden fixtures, {total / 1024:.0f} KiB")
 
