@@ -606,12 +606,18 @@ struct BwdPixel {
     unsigned nexact;
 };
 
+// For the Gaussian dw/dm = -ln2 w, so z = -ln2 o y: only y is exchanged and sweep 2 scales its
+// moments by -ln2 o once per entry.
+template <int FAM>
+struct BwdExchange {
+    static constexpr bool kPair = FAM != FAM_GAUSS2;
+};
+
 template <int FAM, bool CAREFUL>
 __device__ __forceinline__ void bwd_visit(const KParams& kp, const float4* __restrict__ recs,
                                           const float4* __restrict__ qe, float fx, float fy,
                                           BwdPixel& px, float* __restrict__ xw,
-                                          float* __restrict__ xy, float* __restrict__ xz,
-                                          bool& near_acc) {
+                                          float* __restrict__ xyz, bool& near_acc) {
     const float4 s0 = qe[0];
     const float4 s1 = qe[1];
     const float4 s2 = qe[2];
@@ -649,8 +655,10 @@ __device__ __forceinline__ void bwd_visit(const KParams& kp, const float4* __res
     const float d_alpha = fmaf(t_before, gc, -(rc * px.s));
     const float da = gate ? d_alpha : 0.f;
     *xw = wgt;
-    *xy = da * w;
-    *xz = da * s1.y * dwdm;
+    if constexpr (BwdExchange<FAM>::kPair)
+        *reinterpret_cast<float2*>(xyz) = make_float2(da * w, da * s1.y * dwdm);
+    else
+        *xyz = da * w;
     px.s = fmaf(gc, wgt, px.s);
     if (hit) px.T = t_before;
 }
@@ -664,7 +672,8 @@ render_bwd_kernel(KParams kp, const float4* __restrict__ recs, const int2* __res
                   float* __restrict__ grads, unsigned long long* __restrict__ counters) {
     __shared__ __align__(128) float4 ring[kBwdWarps][kStages][kChunkVecs];
     __shared__ unsigned long long bars[kBwdWarps][kStages];
-    __shared__ float xch[kBwdWarps][3][32 * kXStride];
+    // [0]: wgt, then (y, z) pairs, or y alone for the Gaussian
+    __shared__ __align__(16) float xch[kBwdWarps][BwdExchange<FAM>::kPair ? 3 : 2][32 * kXStride];
     __shared__ float4 gpix[kBwdWarps][32];
     const int tile = blockIdx.x >> 1, half = blockIdx.x & 1;
     const int warp = __reduce_min_sync(kFull, (int)(threadIdx.x >> 5)), lane = threadIdx.x & 31;
@@ -694,22 +703,21 @@ render_bwd_kernel(KParams kp, const float4* __restrict__ recs, const int2* __res
     if (__reduce_max_sync(kFull, px.nproc) == 0) return;
     px.s = (px.g0 * bg0 + px.g1 * bg1 + px.g2 * bg2) * px.T;
 
+    constexpr bool kPair = BwdExchange<FAM>::kPair;
+    constexpr int kYzWords = kPair ? 2 : 1;  // floats per (pixel, entry) slot of the second array
     float4* gp = gpix[warp];
     float* xw = xch[warp][0];
-    float* xy = xch[warp][1];
-    float* xz = xch[warp][2];
-    gp[lane] = make_float4(px.g0, px.g1, px.g2, 0.f);
+    float* xyz = xch[warp][1];
+    gp[lane] = make_float4(px.g0, px.g1, px.g2, 1.f);  // .w = 1 accumulates the weight sum
 
     // sweep-2 role of this lane: entry sj of the batch, pixels [16 sh, 16 sh + 16)
     const int sj = lane & (kBwdBatch - 1), sh = lane >> 4;
     const float* rw = xw + (sh * 16) * kXStride + sj;
-    const float* ry = xy + (sh * 16) * kXStride + sj;
-    const float* rz = xz + (sh * 16) * kXStride + sj;
+    const float* ryz = xyz + kYzWords * ((sh * 16) * kXStride + sj);
     const float4* rg = gp + sh * 16;
     const float ex0 = X0, ey0 = Y0 + 2.f * sh;
     float* ww = xw + lane * kXStride;
-    float* wy = xy + lane * kXStride;
-    float* wz = xz + lane * kXStride;
+    float* wyz = xyz + kYzWords * (lane * kXStride);
 
     // The entries the forward composited, [0, used), chunk by chunk from the last.  Entries of the
     // last batch beyond `used` (the stream is padded to a whole chunk) and entries past the last
@@ -745,13 +753,13 @@ render_bwd_kernel(KParams kp, const float4* __restrict__ recs, const int2* __res
                 bool near_acc = false;
 #pragma unroll
                 for (int j = kGroup - 1; j >= 0; --j)
-                    bwd_visit<FAM, false>(kp, recs, qb + (j0 + j) * 3, fx, fy, px, ww + j0 + j, wy + j0 + j,
-                                          wz + j0 + j, near_acc);
+                    bwd_visit<FAM, false>(kp, recs, qb + (j0 + j) * 3, fx, fy, px, ww + j0 + j,
+                                          wyz + kYzWords * (j0 + j), near_acc);
                 if (kp.exact && __any_sync(kFull, near_acc)) {  // a few groups per thousand
                     px = save;
                     for (int j = kGroup - 1; j >= 0; --j)
-                        bwd_visit<FAM, true>(kp, recs, qb + (j0 + j) * 3, fx, fy, px, ww + j0 + j, wy + j0 + j,
-                                             wz + j0 + j, near_acc);
+                        bwd_visit<FAM, true>(kp, recs, qb + (j0 + j) * 3, fx, fy, px, ww + j0 + j,
+                                             wyz + kYzWords * (j0 + j), near_acc);
                 }
             }
             __syncwarp();
@@ -760,28 +768,35 @@ render_bwd_kernel(KParams kp, const float4* __restrict__ recs, const int2* __res
                 const float4 r0 = qb[sj * 3 + 0];
                 const float4 r1 = qb[sj * 3 + 1];
                 const float4 r2 = qb[sj * 3 + 2];
-                const float ex = ex0 - r0.x, ey = ey0 - r0.y;
-                float dc0 = 0.f, dc1 = 0.f, dc2 = 0.f, dop = 0.f, wsum = 0.f;
-                float sxx = 0.f, sxy = 0.f, syy = 0.f, sx = 0.f, sy = 0.f;
+                // packed FP32 (fma.rn.f32x2): two accumulators per instruction
+                float2 dxy = make_float2(ex0 - r0.x, ey0 - r0.y);
+                float2 dc01 = make_float2(0.f, 0.f), dc2w = dc01, sxxxy = dc01, sxsy = dc01;
+                float syy = 0.f, dop = 0.f;
+                const float2 step_x = make_float2(1.f, 0.f), step_row = make_float2(-7.f, 1.f);
 #pragma unroll
                 for (int i = 0; i < 16; ++i) {
                     const float wv = rw[i * kXStride];
-                    const float yv = ry[i * kXStride];
-                    const float zv = rz[i * kXStride];
+                    float yv, zv;
+                    if constexpr (kPair) {
+                        const float2 yz = *reinterpret_cast<const float2*>(ryz + 2 * i * kXStride);
+                        yv = yz.x;
+                        zv = yz.y;
+                    } else {
+                        yv = zv = ryz[i * kXStride];
+                    }
                     const float4 g = rg[i];
-                    const float dx = ex + (float)(i & 7), dy = ey + (float)(i >> 3);
-                    dc0 = fmaf(g.x, wv, dc0);
-                    dc1 = fmaf(g.y, wv, dc1);
-                    dc2 = fmaf(g.z, wv, dc2);
-                    wsum += wv;
+                    const float2 wv2 = make_float2(wv, wv);
+                    dc01 = __ffma2_rn(wv2, make_float2(g.x, g.y), dc01);
+                    dc2w = __ffma2_rn(wv2, make_float2(g.z, g.w), dc2w);
+                    const float2 zxy = __fmul2_rn(make_float2(zv, zv), dxy);  // z (dx, dy)
+                    sxxxy = __ffma2_rn(make_float2(zxy.x, zxy.x), dxy, sxxxy);
+                    sxsy = __fadd2_rn(sxsy, zxy);
+                    syy = fmaf(zxy.y, dxy.y, syy);
                     dop += yv;
-                    const float zx = zv * dx, zy = zv * dy;
-                    sxx = fmaf(zx, dx, sxx);
-                    sxy = fmaf(zx, dy, sxy);
-                    syy = fmaf(zy, dy, syy);
-                    sx += zx;
-                    sy += zy;
+                    dxy = __fadd2_rn(dxy, (i & 7) == 7 ? step_row : step_x);
                 }
+                float dc0 = dc01.x, dc1 = dc01.y, dc2 = dc2w.x, wsum = dc2w.y;
+                float sxx = sxxxy.x, sxy = sxxxy.y, sx = sxsy.x, sy = sxsy.y;
                 // fold the two pixel halves (lanes l and l ^ 16 hold the same entry)
                 dc0 += __shfl_xor_sync(kFull, dc0, 16);
                 dc1 += __shfl_xor_sync(kFull, dc1, 16);
@@ -793,6 +808,14 @@ render_bwd_kernel(KParams kp, const float4* __restrict__ recs, const int2* __res
                 syy += __shfl_xor_sync(kFull, syy, 16);
                 sx += __shfl_xor_sync(kFull, sx, 16);
                 sy += __shfl_xor_sync(kFull, sy, 16);
+                if constexpr (!kPair) {  // the moments were taken of y: z = -ln2 o y
+                    const float zs = -0.6931471805599453f * r1.y;
+                    sxx *= zs;
+                    sxy *= zs;
+                    syy *= zs;
+                    sx *= zs;
+                    sy *= zs;
+                }
                 if (sh == 0 && wsum > 0.f) {
                     // SplatGrads order d_color[3], d_opacity, d_conic_a, d_conic_b, d_conic_c, d_mu2;
                     // m = scale * (a dx^2 + 2 b dx dy + c dy^2): dm/da = scale dx^2, dm/db = 2 scale dx dy,
