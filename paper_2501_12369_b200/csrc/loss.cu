@@ -396,10 +396,19 @@ ssim_grad_kernel(Window win, int w, int h, const float* __restrict__ image,
 // sum_d k[d] [reflect(i + d) == j] (loss.cpp:76-103); every source of a border position lies
 // within five of it (also after repeated reflection in images narrower than the window).
 __device__ __forceinline__ float adjoint_weight(const Window& win, int i, int j, int n) {
+    if (i < 0 || i >= n) return 0.f;
     float acc = 0.f;
-    if (i >= 0 && i < n)
+    if (n >= 2 * kHalf) {
+        // one reflection at most: position p = i + d lands on j directly, through the left edge
+        // (p = -j - 1) or through the right edge (p = 2n - 1 - j)
+        const int d0 = j - i, d1 = -j - 1 - i, d2 = 2 * n - 1 - j - i;
+        if (d0 >= -kHalf && d0 <= kHalf) acc += win.k[d0 + kHalf];
+        if (d1 >= -kHalf && d1 <= kHalf) acc += win.k[d1 + kHalf];
+        if (d2 >= -kHalf && d2 <= kHalf) acc += win.k[d2 + kHalf];
+    } else {
         for (int d = -kHalf; d <= kHalf; ++d)
             if (reflect(i + d, n) == j) acc += win.k[d + kHalf];
+    }
     return acc;
 }
 

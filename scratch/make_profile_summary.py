@@ -49,13 +49,12 @@ for r in rows[2:]:
                 pass
             lines.append(f"| {label} | {v} {units[hdr.index(k)]} |")
     lines.append("")
-src = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--kernel-name", "regex:" + kre],
-                     capture_output=True, text=True).stdout
+src = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv"], capture_output=True, text=True).stdout
 done = set()
 for b in re.split(r'(?m)^"Kernel Name",', src)[1:]:
     ls = list(csv.reader(io.StringIO(b)))
     name = ls[0][0]
-    if name in done:
+    if name in done or not re.search(kre, name):
         continue
     done.add(name)
     h = ls[1]

@@ -18,7 +18,7 @@ p = torch.from_numpy(init).to(dev); g = torch.zeros_like(p); m = torch.zeros(14 
 ctx.set_stage_timing(True)
 for it in range(4):
     g.zero_()
-    loss = ctx.evaluate_view(k, psi, p, cam, (0, 0, 0), target=target, lam=0.0, param_grads=g)
+    loss = ctx.evaluate_view(k, psi, p, cam, (0, 0, 0), target=target, lam=0.2, param_grads=g)
     t = ctx.stage_times()
     ctx.adam_step(p.view(-1), g.view(-1), m, v, lrs, it + 1)
     t["adam"] = ctx.stage_times()["adam"]
