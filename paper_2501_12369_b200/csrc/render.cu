@@ -451,20 +451,26 @@ __device__ __forceinline__ void fwd_visit(const KParams& kp, const float4* __res
     px.T = Tn;
 }
 
+// Warps of a forward CTA.  A warp owns one 8x4 block and leaves as soon as its 32 pixels have
+// saturated; with a whole tile (8 warps) per CTA the early leavers' slots idle until the CTA's
+// slowest warp is done, so CTAs are kept small and the hardware scheduler backfills.
+constexpr int kFwdWarps = 2;
+
 template <int FAM>
-__global__ void __launch_bounds__(kThreads, 4)
+__global__ void __launch_bounds__(32 * kFwdWarps, 32 / kFwdWarps)
 render_fwd_kernel(KParams kp, const float4* __restrict__ recs, const int2* __restrict__ ranges,
                   const int* __restrict__ point_list, const float4* __restrict__ streams,
                   const int* __restrict__ stream_count, int* __restrict__ stream_used, int W, int H,
                   int tiles_x, float bg0, float bg1, float bg2, float* __restrict__ image,
                   float* __restrict__ t_final, int* __restrict__ processed, int* __restrict__ contributors,
                   unsigned long long* __restrict__ counters) {
-    __shared__ __align__(128) float4 ring[kWarpsPerCta][kStages][kChunkVecs];
-    __shared__ unsigned long long bars[kWarpsPerCta][kStages];
-    const int tile = blockIdx.x;
+    __shared__ __align__(128) float4 ring[kFwdWarps][kStages][kChunkVecs];
+    __shared__ unsigned long long bars[kFwdWarps][kStages];
     // the warp index through a warp reduction: the compiler then knows it is warp-uniform and
     // keeps the ring pointers and loop control in uniform registers
-    const int warp = __reduce_min_sync(kFull, (int)(threadIdx.x >> 5)), lane = threadIdx.x & 31;
+    const int lwarp = __reduce_min_sync(kFull, (int)(threadIdx.x >> 5)), lane = threadIdx.x & 31;
+    const int gwarp = blockIdx.x * kFwdWarps + lwarp;
+    const int tile = gwarp / kBlocksPerTile, warp = gwarp % kBlocksPerTile;  // warp: the block inside the tile
     const int bx = (tile % tiles_x) * DARBS_TILE_SIZE + (warp & 1) * 8;
     const int by = (tile / tiles_x) * DARBS_TILE_SIZE + (warp >> 1) * 4;
     if (bx >= W || by >= H) return;  // whole block outside the image
@@ -484,8 +490,8 @@ render_fwd_kernel(KParams kp, const float4* __restrict__ recs, const int2* __res
     const float4* src = streams + kEntryVecs * stream_offset(tile, beg, end, warp);
     const int n = stream_count[tile * kBlocksPerTile + warp];
     const int nchunks = (n + kChunk - 1) / kChunk;
-    float4* stage0 = ring[warp][0];
-    unsigned long long* bar = bars[warp];
+    float4* stage0 = ring[lwarp][0];
+    unsigned long long* bar = bars[lwarp];
     if (lane == 0) {
         for (int s = 0; s < kStages; ++s) mbar_init(bar + s);
         mbar_init_fence();
@@ -578,8 +584,9 @@ render_fwd_kernel(KParams kp, const float4* __restrict__ recs, const int2* __res
 
 // ----------------------------------------------------------------- backward
 //
-// One CTA of 4 warps per HALF tile (16x8 pixels); a warp owns an 8x4 block as in
-// the forward and walks the part of its stream the forward composited, from the
+// One single-warp CTA per 8x4 block (warps need nothing from each other, and with several
+// blocks to a CTA the early finishers' slots idle until the slowest is done: measured 6-9 %
+// slower at 4 warps per CTA for the families whose pixels saturate early); the warp walks the part of its stream the forward composited, from the
 // back, in two sweeps per batch of kBwdBatch entries:
 //   sweep 1 (lane = pixel): the reverse compositing chain of rasterizer.cpp:
 //       189-213; per (pixel, entry) it leaves three numbers in a padded
@@ -592,7 +599,7 @@ render_fwd_kernel(KParams kp, const float4* __restrict__ recs, const int2* __res
 //       No per-entry cross-lane reduction.
 // Then two 128-bit and one 32-bit red.global.add per entry into gradient rows
 // padded to 12 floats.
-constexpr int kBwdWarps = 4;
+constexpr int kBwdWarps = 1;
 constexpr int kBwdThreads = 32 * kBwdWarps;
 constexpr int kBwdBatch = 16;
 constexpr int kXStride = kBwdBatch + 1;  // odd: conflict-free both by row and by column
@@ -664,7 +671,7 @@ __device__ __forceinline__ void bwd_visit(const KParams& kp, const float4* __res
 }
 
 template <int FAM>
-__global__ void __launch_bounds__(kBwdThreads, 4)
+__global__ void __launch_bounds__(kBwdThreads, 16 / kBwdWarps)
 render_bwd_kernel(KParams kp, const float4* __restrict__ recs, const int2* __restrict__ ranges,
                   const float4* __restrict__ streams, const int* __restrict__ stream_used, int W, int H,
                   int tiles_x, float bg0, float bg1, float bg2, const float* __restrict__ grad_image,
@@ -675,11 +682,11 @@ render_bwd_kernel(KParams kp, const float4* __restrict__ recs, const int2* __res
     // [0]: wgt, then (y, z) pairs, or y alone for the Gaussian
     __shared__ __align__(16) float xch[kBwdWarps][BwdExchange<FAM>::kPair ? 3 : 2][32 * kXStride];
     __shared__ float4 gpix[kBwdWarps][32];
-    const int tile = blockIdx.x >> 1, half = blockIdx.x & 1;
     const int warp = __reduce_min_sync(kFull, (int)(threadIdx.x >> 5)), lane = threadIdx.x & 31;
-    const int blk = half * kBwdWarps + warp;  // the forward's warp index of this block
-    const int bx = (tile % tiles_x) * DARBS_TILE_SIZE + (warp & 1) * 8;
-    const int by = (tile / tiles_x) * DARBS_TILE_SIZE + half * 8 + (warp >> 1) * 4;
+    const int gwarp = blockIdx.x * kBwdWarps + warp;
+    const int tile = gwarp / kBlocksPerTile, blk = gwarp % kBlocksPerTile;  // blk: the forward's block index
+    const int bx = (tile % tiles_x) * DARBS_TILE_SIZE + (blk & 1) * 8;
+    const int by = (tile / tiles_x) * DARBS_TILE_SIZE + (blk >> 1) * 4;
     if (bx >= W || by >= H) return;
     const int pxl = bx + (lane & 7), pyl = by + (lane >> 3);
     const bool inside = pxl < W && pyl < H;
@@ -945,7 +952,7 @@ darbs_status launch_render_fwd(darbs_cuda_ctx* ctx, const KParams& kp, int width
     const int* count = (const int*)ctx->stream_count.ptr;
     int* used = (int*)ctx->stream_count.ptr + (size_t)kBlocksPerTile * tiles;
 #define DARBS_LAUNCH_FWD(F)                                                                       \
-    render_fwd_kernel<F><<<tiles, kThreads, 0, ctx->stream>>>(                                    \
+    render_fwd_kernel<F><<<tiles * (kBlocksPerTile / kFwdWarps), 32 * kFwdWarps, 0, ctx->stream>>>(  \
         kp, recs, ranges, plist, (const float4*)ctx->streams.ptr, count, used, width, height,     \
         ctx->tiles_x, bg[0], bg[1], bg[2], image, t_final, processed, contributors, counters)
     switch (kp.fam) {
@@ -974,7 +981,7 @@ darbs_status launch_render_bwd(darbs_cuda_ctx* ctx, const KParams& kp, int width
     const int2* ranges = (const int2*)ctx->ranges.ptr;
     const int* used = (const int*)ctx->stream_count.ptr + (size_t)kBlocksPerTile * tiles;
 #define DARBS_LAUNCH_BWD(F)                                                                       \
-    render_bwd_kernel<F><<<2 * tiles, kBwdThreads, 0, ctx->stream>>>(                             \
+    render_bwd_kernel<F><<<tiles * (kBlocksPerTile / kBwdWarps), kBwdThreads, 0, ctx->stream>>>(                             \
         kp, recs, ranges, (const float4*)ctx->streams.ptr, used, width, height, ctx->tiles_x,     \
         bg[0], bg[1], bg[2], grad_image, t_final, processed, (float*)ctx->splat_grads.ptr, counters)
     switch (kp.fam) {
