@@ -70,6 +70,8 @@ static int pick_fam(const darbs_kernel_spec& s) {
             return (s.beta == 1.0 && s.lobes == 1) ? FAM_RCOS1 : FAM_GENERIC;
         case DARBS_INVERSE_MULTIQUADRATIC:
             return FAM_IMQ;  // eval ignores beta for this family (kernel.cpp:139-145)
+        case DARBS_MODULUS_SINC:
+            return (s.beta == 1.0 && s.lobes == 1) ? FAM_MSINC1 : FAM_GENERIC;
         default:
             return FAM_GENERIC;
     }

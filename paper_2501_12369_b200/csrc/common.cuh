@@ -15,14 +15,15 @@ namespace darbs_b200 {
 // ---------------------------------------------------------------- families
 // Compile-time specialisations of the DARBF family (kernel.cpp:73-104 /
 // :127-164).  The four presets of the paper get a closed form on the scaled
-// squared distance m = scale * dm2; every other (family, beta, lobes)
-// combination runs through FAM_GENERIC.
+// squared distance m = scale * dm2 (and so does the reference's fifth preset, mod-sinc);
+// every other (family, beta, lobes) combination runs through FAM_GENERIC.
 enum : int {
     FAM_GAUSS2 = 0,   // Gaussian, beta = 2:            w = exp(-dm2/xi)
     FAM_HCOS2 = 1,    // half-cosine, beta = 2:         w = cos(dm2/xi)
     FAM_RCOS1 = 2,    // raised-cosine, beta = 1, 1 lobe: w = .5 + .5 cos(sqrt(dm2)/xi)
     FAM_IMQ = 3,      // inverse multiquadric:          w = 1/sqrt(dm2/xi + 1)
-    FAM_GENERIC = 4   // anything else (mod-sinc, multi-lobe, other beta)
+    FAM_MSINC1 = 4,   // modulus sinc, beta = 1, 1 lobe: w = sin(u)/u, u = sqrt(dm2)/xi in [0, pi]
+    FAM_GENERIC = 5   // anything else (multi-lobe, other beta)
 };
 
 struct KParams {

@@ -52,9 +52,42 @@ __host__ __device__ inline double family_scale(int fam, double xi) {
             return 1.0 / (xi * xi);          // w = .5 + .5 cos(sqrt(m))
         case FAM_IMQ:
             return 1.0 / xi;                 // w = rsqrt(m + 1)
+        case FAM_MSINC1:
+            return 1.0 / (xi * xi);          // w = sin(sqrt(m)) / sqrt(m)
         default:
             return 1.0;
     }
+}
+
+// sin(sqrt(m))/sqrt(m) = sum_k (-m)^k / (2k+1)! on the main lobe m in [0, pi^2]: an entire
+// function of m, so the single-lobe modulus sinc (|sin u| = sin u on [0, pi], kernel.cpp:87-98)
+// needs neither the square root nor a trigonometric call.  Eleven terms leave 2e-10 at m = pi^2;
+// the terms never exceed 1.7, so Horner in FP32 is good to ~2e-7 absolute.
+__device__ __forceinline__ float msinc_poly(float m) {
+    float p = 1.9572941063391263e-20f;                            //  1/21!
+    p = fmaf(p, m, -8.2206352466243297e-18f);                     // -1/19!
+    p = fmaf(p, m, 2.8114572543455208e-15f);                      //  1/17!
+    p = fmaf(p, m, -7.6471637318198165e-13f);                     // -1/15!
+    p = fmaf(p, m, 1.6059043836821613e-10f);                      //  1/13!
+    p = fmaf(p, m, -2.5052108385441719e-08f);                     // -1/11!
+    p = fmaf(p, m, 2.7557319223985893e-06f);                      //  1/9!
+    p = fmaf(p, m, -1.9841269841269841e-04f);                     // -1/7!
+    p = fmaf(p, m, 8.3333333333333333e-03f);                      //  1/5!
+    p = fmaf(p, m, -1.6666666666666666e-01f);                     // -1/3!
+    return fmaf(p, m, 1.0f);
+}
+// d/dm of the series: sum_k (-1)^k k m^(k-1) / (2k+1)!
+__device__ __forceinline__ float msinc_dpoly(float m) {
+    float p = 10.0f * 1.9572941063391263e-20f;
+    p = fmaf(p, m, -9.0f * 8.2206352466243297e-18f);
+    p = fmaf(p, m, 8.0f * 2.8114572543455208e-15f);
+    p = fmaf(p, m, -7.0f * 7.6471637318198165e-13f);
+    p = fmaf(p, m, 6.0f * 1.6059043836821613e-10f);
+    p = fmaf(p, m, -5.0f * 2.5052108385441719e-08f);
+    p = fmaf(p, m, 4.0f * 2.7557319223985893e-06f);
+    p = fmaf(p, m, -3.0f * 1.9841269841269841e-04f);
+    p = fmaf(p, m, 2.0f * 8.3333333333333333e-03f);
+    return fmaf(p, m, -1.6666666666666666e-01f);
 }
 
 // FP32 weight and derivative with respect to m (NOT dm2) for m inside the
@@ -76,6 +109,9 @@ __device__ __forceinline__ void fam_eval(float m, float& w, float& dwdm) {
         float r = rsqrt_approx(m + 1.0f);
         w = r;
         dwdm = -0.5f * r * r * r;
+    } else if constexpr (FAM == FAM_MSINC1) {
+        w = fminf(fmaxf(msinc_poly(m), 0.f), 1.f);  // kernel.cpp:161 clamps f to [0, 1]
+        dwdm = msinc_dpoly(m);
     } else {
         w = 0.f;
         dwdm = 0.f;
@@ -92,6 +128,8 @@ __device__ __forceinline__ float fam_weight(float m) {
         return fmaf(0.5f, __cosf(sqrt_approx(fmaxf(m, 0.f))), 0.5f);
     } else if constexpr (FAM == FAM_IMQ) {
         return rsqrt_approx(m + 1.0f);
+    } else if constexpr (FAM == FAM_MSINC1) {
+        return fminf(fmaxf(msinc_poly(m), 0.f), 1.f);
     } else {
         return 0.f;
     }
@@ -210,6 +248,22 @@ __device__ inline double family_threshold(const KParams& kp, double o) {
         case FAM_IMQ:
             thr = t > 1.0 ? -1.0 : kp.xi_d * (1.0 / (t * t) - 1.0);
             break;
+        case FAM_MSINC1: {
+            // sin(u)/u = t on [0, pi] (monotone): Newton from the two-term series u0 = sqrt(6 (1 - t)).
+            // The result only has to land inside the guard band, where decisions are re-taken exactly.
+            if (t > 1.0) {
+                thr = -1.0;
+            } else {
+                double u = fmin(sqrt(6.0 * (1.0 - t)), kPiD);
+                for (int it = 0; it < 6 && u > 1e-6; ++it) {
+                    const double su = sin(u), cu = cos(u);
+                    const double f = su / u - t, df = (u * cu - su) / (u * u);
+                    u = fmin(fmax(u - f / df, 0.0), kPiD);
+                }
+                thr = (kp.xi_d * u) * (kp.xi_d * u);
+            }
+            break;
+        }
         default:
             thr = kp.cutoff_d;
             break;

@@ -399,7 +399,8 @@ constexpr int kGroup = 8;  // entries composited speculatively between two guard
 // (rasterizer.cpp:100 leaves the loop the first time T < 1e-4); lanes outside
 // the image start at T = 0 and never take a splat.
 struct FwdPixel {
-    float T, cr, cg, cb;
+    float2 crg;  // red and green accumulate in one packed FMA
+    float T, cb;
     float contrib;  // contributor count, kept in FP32 (exact below 2^24) so a hit costs one FADD
     int proc;
     unsigned nexact;
@@ -420,7 +421,9 @@ __device__ __forceinline__ void fwd_visit(const KParams& kp, const float4* __res
     const float4 s0 = qe[0];
     const float4 s1 = qe[1];
     const float4 s2 = qe[2];
-    const float dx = fx - s0.x, dy = fy - s0.y;
+    // (mu - centre): the quadratic form is even, and the packed add takes no negated operand
+    const float2 d = __fadd2_rn(make_float2(s0.x, s0.y), make_float2(-fx, -fy));
+    const float dx = d.x, dy = d.y;
     const float m = quad_m(s0.z, s0.w, s1.x, dx, dy);
     const bool live = !(px.T < kTFloorF);
     bool hit, near;
@@ -441,8 +444,7 @@ __device__ __forceinline__ void fwd_visit(const KParams& kp, const float4* __res
     alpha *= hitf;
     // rasterizer.cpp:96-100
     const float at = alpha * px.T;
-    px.cr = fmaf(s2.x, at, px.cr);
-    px.cg = fmaf(s2.y, at, px.cg);
+    px.crg = __ffma2_rn(make_float2(s2.x, s2.y), make_float2(at, at), px.crg);
     px.cb = fmaf(s2.z, at, px.cb);
     const float Tn = fmaf(-alpha, px.T, px.T);
     px.contrib += hitf;
@@ -482,7 +484,8 @@ render_fwd_kernel(KParams kp, const float4* __restrict__ recs, const int2* __res
 
     FwdPixel px;
     px.T = inside ? 1.f : 0.f;
-    px.cr = px.cg = px.cb = 0.f;
+    px.crg = make_float2(0.f, 0.f);
+    px.cb = 0.f;
     px.contrib = 0.f;
     px.proc = end - beg;
     px.nexact = 0;
@@ -564,8 +567,8 @@ render_fwd_kernel(KParams kp, const float4* __restrict__ recs, const int2* __res
             nfloor = nfloor || fabsf(t_cross - kTFloorF) < 4e-9f;
         }
         size_t p = (size_t)pyl * W + pxl;
-        image[p * 3 + 0] = fmaf(bg0, px.T, px.cr);
-        image[p * 3 + 1] = fmaf(bg1, px.T, px.cg);
+        image[p * 3 + 0] = fmaf(bg0, px.T, px.crg.x);
+        image[p * 3 + 1] = fmaf(bg1, px.T, px.crg.y);
         image[p * 3 + 2] = fmaf(bg2, px.T, px.cb);
         t_final[p] = px.T;
         processed[p] = px.proc;
@@ -884,6 +887,7 @@ __global__ void eval_kernel(KParams kp, int64_t n, const float* __restrict__ dm2
             case FAM_HCOS2: eval_one_fast<FAM_HCOS2>(kp, x, wo, dwo); break;
             case FAM_RCOS1: eval_one_fast<FAM_RCOS1>(kp, x, wo, dwo); break;
             case FAM_IMQ: eval_one_fast<FAM_IMQ>(kp, x, wo, dwo); break;
+            case FAM_MSINC1: eval_one_fast<FAM_MSINC1>(kp, x, wo, dwo); break;
             default: eval_one_fast<FAM_GENERIC>(kp, x, wo, dwo); break;
         }
     }
@@ -960,6 +964,7 @@ darbs_status launch_render_fwd(darbs_cuda_ctx* ctx, const KParams& kp, int width
         case FAM_HCOS2: DARBS_LAUNCH_FWD(FAM_HCOS2); break;
         case FAM_RCOS1: DARBS_LAUNCH_FWD(FAM_RCOS1); break;
         case FAM_IMQ: DARBS_LAUNCH_FWD(FAM_IMQ); break;
+        case FAM_MSINC1: DARBS_LAUNCH_FWD(FAM_MSINC1); break;
         default: DARBS_LAUNCH_FWD(FAM_GENERIC); break;
     }
 #undef DARBS_LAUNCH_FWD
@@ -989,6 +994,7 @@ darbs_status launch_render_bwd(darbs_cuda_ctx* ctx, const KParams& kp, int width
         case FAM_HCOS2: DARBS_LAUNCH_BWD(FAM_HCOS2); break;
         case FAM_RCOS1: DARBS_LAUNCH_BWD(FAM_RCOS1); break;
         case FAM_IMQ: DARBS_LAUNCH_BWD(FAM_IMQ); break;
+        case FAM_MSINC1: DARBS_LAUNCH_BWD(FAM_MSINC1); break;
         default: DARBS_LAUNCH_BWD(FAM_GENERIC); break;
     }
 #undef DARBS_LAUNCH_BWD

@@ -29,6 +29,10 @@ IMG_TOL = 2e-5
 GRAD_TOL = 1e-3
 GRAD_FLOOR = 1e-4
 KERNELS = ["gaussian", "half-cosine-sq", "raised-cosine", "inv-multiquadratic", "mod-sinc"]
+# (family, beta, xi, lobes) outside the presets: multi-lobe and other beta run the generic device
+# path of the render kernels (kernel.cpp:73-104, tests/test_kernel.cpp:153-161)
+GENERIC = ["custom:raised-cosine:1.0:0.6:2", "custom:half-cosine:1.0:1.9:1", "custom:mod-sinc:1.0:0.8:2",
+           "custom:gaussian:1.5:2.0:1"]
 BG = (0.1, 0.2, 0.3)
 
 
@@ -103,16 +107,30 @@ def test_bins_huge_and_offscreen_and_nonfinite(ctx, port):
 _KCACHE = {}
 
 
+def custom_spec(name):
+    _, family, beta, xi, lobes = name.split(":")
+    return family, float(beta), float(xi), int(lobes)
+
+
 def gpu_kernel_cached(name):
     import paper_2501_12369_b200 as d
 
     if name not in _KCACHE:
-        _KCACHE[name] = d.kernel_preset(name)
+        _KCACHE[name] = d.make_kernel(*custom_spec(name)) if name.startswith("custom:") else d.kernel_preset(name)
     return _KCACHE[name]
 
 
+def oracle_kernel(port, name):
+    if not name.startswith("custom:"):
+        return port.preset(name)
+    family, beta, xi, lobes = custom_spec(name)
+    st, k = port.make_kernel(gpu_kernel_cached(name).family, beta, xi, lobes)
+    assert st == 0
+    return k
+
+
 def run_forward_parity(ctx, port, name, n, w, h, seed, bg=BG):
-    k = port.preset(name)
+    k = oracle_kernel(port, name)
     s = port.random_scene(k, n, w, h, seed)
     ref = port.forward(k, s, w, h, bg, threads=0)
     out = ctx.forward(gpu_kernel_cached(name), **scene_f32(s), width=w, height=h, background=bg)
@@ -143,7 +161,7 @@ def test_forward_equals_bruteforce_oracle(ctx, port, name):
         assert np.abs(out["image"] - brute).max() <= IMG_TOL
 
 
-@pytest.mark.parametrize("name", KERNELS)
+@pytest.mark.parametrize("name", KERNELS + GENERIC)
 def test_forward_parity_ragged_dense(ctx, port, name):
     """Image not a multiple of the tile size, lists longer than one 32-entry chunk, early
     termination on most pixels."""
@@ -221,7 +239,7 @@ def grad_err(got, ref):
 
 
 def run_backward_parity(ctx, port, name, n, w, h, seed, gseed=32):
-    k = port.preset(name)
+    k = oracle_kernel(port, name)
     s = port.random_scene(k, n, w, h, seed)
     g = port.random_image_grad(w, h, gseed)
     fr = port.forward(k, s, w, h, BG, threads=0, keep=True)
@@ -249,7 +267,7 @@ def test_backward_parity_small(ctx, port, name, seed):
     run_backward_parity(ctx, port, name, 200, 64, 64, seed)
 
 
-@pytest.mark.parametrize("name", KERNELS)
+@pytest.mark.parametrize("name", KERNELS + GENERIC)
 def test_backward_parity_ragged_dense(ctx, port, name):
     run_backward_parity(ctx, port, name, 3000, 77, 45, 11)
 
