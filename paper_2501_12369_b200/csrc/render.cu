@@ -190,9 +190,13 @@ __device__ __forceinline__ float quad_m(float A, float B, float C, float dx, flo
 // One stream entry = three float4 (48 B).  A chunk = 32 entries = 1536 B, the unit
 // of the bulk copies.  Streams are padded with null entries (zero opacity, threshold
 // -inf, position past every list, splat index -1: nothing can take them) up to a
-// whole chunk, so the compositing loops never see a partial group.
+// multiple of kPad entries, the coarsest unit a compositing loop touches (the forward
+// works in groups of 8, the backward in batches of 16), so no loop ever sees a partial
+// group.  The bulk copies still move whole chunks; what lies between the padding and the
+// end of the chunk is never interpreted.
 constexpr int kEntryVecs = 3;
 constexpr int kChunk = 32;
+constexpr int kPad = 16;
 constexpr int kChunkVecs = kChunk * kEntryVecs;
 constexpr int kChunkBytes = kChunkVecs * (int)sizeof(float4);
 constexpr int kStages = 3;
@@ -351,7 +355,7 @@ cull_kernel(KParams kp, const float4* __restrict__ recs, const int2* __restrict_
     __syncthreads();
     {
         const int b = warp, n = total[b];
-        const int padded = (n + kChunk - 1) & ~(kChunk - 1);
+        const int padded = (n + kPad - 1) & ~(kPad - 1);
         if (n + lane < padded) store_null_entry(tile_streams + kEntryVecs * ((size_t)b * cap + (size_t)(n + lane)));
     }
 }
@@ -605,6 +609,7 @@ render_fwd_kernel(KParams kp, const float4* __restrict__ recs, const int2* __res
 constexpr int kBwdWarps = 1;
 constexpr int kBwdThreads = 32 * kBwdWarps;
 constexpr int kBwdBatch = 16;
+static_assert(kPad % kBwdBatch == 0 && kPad % kGroup == 0 && kChunk % kPad == 0, "stream padding covers every loop unit");
 constexpr int kXStride = kBwdBatch + 1;  // odd: conflict-free both by row and by column
 constexpr int kSplatGradStride = 12;     // internal gradient rows are padded to 12 floats for 128-bit atomics
 
@@ -730,7 +735,7 @@ render_bwd_kernel(KParams kp, const float4* __restrict__ recs, const int2* __res
     float* wyz = xyz + kYzWords * (lane * kXStride);
 
     // The entries the forward composited, [0, used), chunk by chunk from the last.  Entries of the
-    // last batch beyond `used` (the stream is padded to a whole chunk) and entries past the last
+    // last batch beyond `used` (the stream is padded to a whole batch) and entries past the last
     // position a pixel processed are simply not eligible for that pixel.
     const float4* src = streams + kEntryVecs * stream_offset(tile, range.x, range.y, blk);
     const int used = stream_used[tile * kBlocksPerTile + blk];
