@@ -813,10 +813,14 @@ darbs_status darbs_cuda_evaluate_view(darbs_cuda_ctx* ctx, const darbs_kernel_sp
     if (staged >= 0) DARBS_CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->stream, ctx->target_done[staged], 0));
     if (target) {
         StageScope ts(ctx, ST_LOSS);
-        DARBS_TRY(reserve(ctx, ctx->grad_image, sizeof(float) * 3 * px));
-        DARBS_TRY(launch_loss(ctx, width, height, d_image, d_target, lambda, (float*)ctx->grad_image.ptr,
-                              d_sums));
-        d_gimg = (const float*)ctx->grad_image.ptr;
+        // without param_grads nothing consumes dL/dimage: values only (fit_scene's evaluate(false), fit3d.cpp:131)
+        float* d_lgrad = nullptr;
+        if (param_grads) {
+            DARBS_TRY(reserve(ctx, ctx->grad_image, sizeof(float) * 3 * px));
+            d_lgrad = (float*)ctx->grad_image.ptr;
+        }
+        DARBS_TRY(launch_loss(ctx, width, height, d_image, d_target, lambda, d_lgrad, d_sums));
+        d_gimg = d_lgrad;
     }
     if (param_grads) {
         {

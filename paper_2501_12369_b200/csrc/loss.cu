@@ -260,8 +260,10 @@ ssim_map_kernel(Window win, int w, int h, const float* __restrict__ image,
             const float a1 = 2.f * mu_x * mu_y + c1;
             const float a2 = 2.f * (var_x - cov_xd) + c2;       // 2 cov_xy + C2
             const float b1 = a1 + m, b2 = a2 + v;
-            const float inv_b2 = __frcp_rn(b2);
-            const float inv = __frcp_rn(b1) * inv_b2;
+            float inv_b1, inv_b2;  // b1 >= C1, b2 >= C2: one MUFU each, 1 ulp
+            asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(inv_b1) : "f"(b1));
+            asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(inv_b2) : "f"(b2));
+            const float inv = inv_b1 * inv_b2;
             const float one_minus_s = (a1 * v + a2 * m + m * v) * inv;
             const float s = 1.0f - one_minus_s;
             const float d = xc[e] - yc[e];  // 0 past `valid` (load12)
