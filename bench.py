@@ -495,7 +495,18 @@ def cpu_baseline(args):
             total += dt
             iters += 1
     value = iters / total / SAMPLE_FRACTION
+    # the same sample on ONE host thread (SURVEY 8d asks for both): one iteration of the cheapest kernel
+    name = "half-cosine-sq"
+    target = cpu_target(orc, cpu, name, truth, cam, threads)
+    raw = init.astype(np.float64).copy()
+    state = {"m": np.zeros(raw.size), "v": np.zeros(raw.size), "t": 0}
+    dt1, _v = cpu_iteration(orc, cpu, name, raw, cam, target, lrs.astype(np.float64), state, 1)
+    raw = init.astype(np.float64).copy()
+    state = {"m": np.zeros(raw.size), "v": np.zeros(raw.size), "t": 0}
+    dtn, _v = cpu_iteration(orc, cpu, name, raw, cam, target, lrs.astype(np.float64), state, threads)
     return {"value": value, "unit": UNIT, "cores": threads, "kind": kind,
+            "single_thread": {"kernel": name, "iters_per_s_full_equiv": 1.0 / dt1 / SAMPLE_FRACTION,
+                              "all_threads_iters_per_s_full_equiv": 1.0 / dtn / SAMPLE_FRACTION},
             "sample": f"1/{SAMPLE_FRACTION} of the workload at equal splat density ({smp['n']} primitives, "
                       f"{smp['width']}x{smp['height']}), {iters} full training iterations over the 4 kernels, "
                       f"value scaled by 1/{SAMPLE_FRACTION}"}

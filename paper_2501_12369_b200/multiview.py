@@ -75,10 +75,11 @@ class ViewParallelTrainer:
         return self.reduce_loss(sums) if want_loss else None
 
 
-def bind_context(ctx, kernel, psi: float, cameras, targets, background=(0.0, 0.0, 0.0), lam: float = 0.0,
+def bind_context(ctx, kernel, psi: float, cameras, targets, background=(0.0, 0.0, 0.0), lam: float = 0.2,
                  want_loss: bool = True):
     """(evaluate, adam) that run on a :class:`paper_2501_12369_b200.Context` through the C ABI.
-    ``targets[v]`` may be a CUDA tensor (device-resident) or a pinned host array (DARBS_HOST)."""
+    ``targets[v]`` may be a CUDA tensor (device-resident) or a pinned host array (DARBS_HOST);
+    ``lam`` defaults to FitConfig::lambda (include/darbs/fit_common.hpp:16)."""
 
     def evaluate(view, params, grads):
         tgt = targets[view]
