@@ -258,15 +258,18 @@ void reset_stage_marks(darbs_cuda_ctx* ctx, std::initializer_list<int> stages) {
 darbs_status forward_device(darbs_cuda_ctx* ctx, const KParams& kp, int64_t n, const float* mu2,
                             const float* conic, const float* radius, const float* depth,
                             const float* opacity, const float* rgb, const int32_t* valid, int width,
-                            int height, const float bg[3], float* image, int32_t* contributors) {
+                            int height, const float bg[3], float* image, int32_t* contributors,
+                            bool preprocessed = false) {
+    // preprocessed: the fused preprocess of evaluate_view already left the tile rectangles, depth
+    // keys and packed records (binning_begin's sinks), so rect_kernel and pack_kernel are skipped
     const size_t px = (size_t)width * height;
     {
         StageScope ts(ctx, ST_BINNING);
-        DARBS_TRY(run_binning(ctx, n, mu2, conic, radius, depth, valid, width, height));
+        DARBS_TRY(run_binning(ctx, n, mu2, conic, radius, depth, valid, width, height, preprocessed));
     }
     {
         StageScope ts(ctx, ST_CULL);
-        DARBS_TRY(launch_pack(ctx, kp, n, mu2, conic, opacity, rgb));
+        if (!preprocessed) DARBS_TRY(launch_pack(ctx, kp, n, mu2, conic, opacity, rgb));
         DARBS_TRY(launch_cull(ctx, kp));
     }
     // prefetched uploads may start here: from now on the stream holds a few long kernels, whose
@@ -800,15 +803,19 @@ darbs_status darbs_cuda_evaluate_view(darbs_cuda_ctx* ctx, const darbs_kernel_sp
     {
         StageScope ts(ctx, ST_PREPROCESS);
         DARBS_CUDA_TRY(ctx, cudaMemsetAsync(d_flags, 0, sizeof(int) * 2, ctx->stream));
+        SplatSinks sinks;
+        DARBS_TRY(binning_begin(ctx, n, width, height, &sinks));
+        DARBS_TRY(reserve(ctx, ctx->recs, sizeof(float4) * kRecVecs * nn));
+        sinks.recs = (float4*)ctx->recs.ptr;
         DARBS_TRY(launch_project(ctx, kp, psi, DARBS_DILATION, n, d_raw, true, cam, d_valid, d_mu2,
-                                 nullptr, d_conic, d_radius, d_depth, d_opacity, d_rgb, d_flags));
+                                 nullptr, d_conic, d_radius, d_depth, d_opacity, d_rgb, d_flags, &sinks));
     }
     if (!d_image) {
         DARBS_TRY(reserve(ctx, ctx->image, sizeof(float) * 3 * px));
         d_image = (float*)ctx->image.ptr;
     }
     DARBS_TRY(forward_device(ctx, kp, n, d_mu2, d_conic, d_radius, d_depth, d_opacity, d_rgb, d_valid,
-                             width, height, background, d_image, nullptr));
+                             width, height, background, d_image, nullptr, /*preprocessed=*/true));
     DARBS_TRY(sti.await_late());
     if (staged >= 0) DARBS_CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->stream, ctx->target_done[staged], 0));
     if (target) {

@@ -16,7 +16,7 @@
 // (rasterizer.cpp:40-45).
 #include <cub/cub.cuh>
 
-#include "common.cuh"
+#include "splat.cuh"
 
 namespace darbs_b200 {
 
@@ -27,13 +27,6 @@ struct Scalars {  // lives behind the 8 work counters in ctx->counters
     unsigned long long skipped_nonfinite;
 };
 
-__device__ __forceinline__ unsigned depth_to_key(float d) {
-    // order-preserving map float -> uint (negative depths included)
-    unsigned u = __float_as_uint(d);
-    return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
-}
-
-// rect packed as x0 | y0<<16 and x1 | y1<<16 ; touched == 0 -> no tiles
 __global__ void rect_kernel(int64_t n, const float* __restrict__ mu2,
                             const float* __restrict__ conic, const float* __restrict__ radius,
                             const float* __restrict__ depth, const int* __restrict__ valid,
@@ -44,32 +37,10 @@ __global__ void rect_kernel(int64_t n, const float* __restrict__ mu2,
     if (i >= n) return;
     depth_keys[i] = depth_to_key(depth[i]);
     order[i] = (unsigned)i;
-    bool ok = valid ? valid[i] != 0 : true;
-    unsigned cnt = 0;
-    uint2 rect = make_uint2(0, 0);
-    if (ok) {
-        float a = conic[3 * i], b = conic[3 * i + 1], c = conic[3 * i + 2], r = radius[i];
-        if (!(isfinite(a) && isfinite(b) && isfinite(c) && isfinite(r))) {  // rasterizer.cpp:39
-            atomicAdd(&scalars->skipped_nonfinite, 1ull);
-        } else {
-            double mx = mu2[2 * i], my = mu2[2 * i + 1], rd = r;
-            // rasterizer.cpp:40-45 (the clamp happens in floating point here so
-            // that huge coordinates cannot overflow the int conversion)
-            double fx0 = floor((mx - rd) / DARBS_TILE_SIZE), fy0 = floor((my - rd) / DARBS_TILE_SIZE);
-            double fx1 = floor((mx + rd) / DARBS_TILE_SIZE), fy1 = floor((my + rd) / DARBS_TILE_SIZE);
-            // NaN centres compare false everywhere -> empty rect, like an
-            // int-converted NaN would be garbage in the reference (unsupported).
-            if (fx1 >= 0.0 && fy1 >= 0.0 && fx0 <= tiles_x - 1 && fy0 <= tiles_y - 1) {
-                int x0 = (int)fmax(fx0, 0.0), y0 = (int)fmax(fy0, 0.0);
-                int x1 = (int)fmin(fx1, (double)(tiles_x - 1)), y1 = (int)fmin(fy1, (double)(tiles_y - 1));
-                if (x1 >= x0 && y1 >= y0) {
-                    cnt = (unsigned)(x1 - x0 + 1) * (unsigned)(y1 - y0 + 1);
-                    rect = make_uint2((unsigned)x0 | ((unsigned)y0 << 16),
-                                      (unsigned)x1 | ((unsigned)y1 << 16));
-                }
-            }
-        }
-    }
+    uint2 rect;
+    unsigned cnt;
+    splat_rect(valid ? valid[i] != 0 : true, mu2[2 * i], mu2[2 * i + 1], conic[3 * i], conic[3 * i + 1],
+               conic[3 * i + 2], radius[i], tiles_x, tiles_y, &scalars->skipped_nonfinite, rect, cnt);
     rects[i] = rect;
     touched[i] = cnt;
 }
@@ -196,9 +167,9 @@ darbs_status tile_sort(darbs_cuda_ctx* ctx, int64_t n, int64_t k, int tiles, con
     return check_launch(ctx, "ranges_kernel");
 }
 
-darbs_status run_binning(darbs_cuda_ctx* ctx, int64_t n, const float* mu2, const float* conic,
-                         const float* radius, const float* depth, const int32_t* valid,
-                         int width, int height) {
+// Sizes the per-splat buffers of the stage, clears its counters and the tile ranges, and tells
+// where a fused preprocess may leave the rectangles, depth keys and identity order itself.
+darbs_status binning_begin(darbs_cuda_ctx* ctx, int64_t n, int width, int height, SplatSinks* sinks) {
     cudaStream_t s = ctx->stream;
     ctx->tiles_x = (width + DARBS_TILE_SIZE - 1) / DARBS_TILE_SIZE;
     ctx->tiles_y = (height + DARBS_TILE_SIZE - 1) / DARBS_TILE_SIZE;
@@ -214,6 +185,7 @@ darbs_status run_binning(darbs_cuda_ctx* ctx, int64_t n, const float* mu2, const
     ctx->fwd_entries = 0;
     ctx->cur_key_buf = 0;
     ctx->cur_order_buf = 0;
+    if (sinks) *sinks = SplatSinks();
     if (n == 0 || tiles == 0) return DARBS_OK;
 
     const size_t nn = (size_t)n;
@@ -221,6 +193,28 @@ darbs_status run_binning(darbs_cuda_ctx* ctx, int64_t n, const float* mu2, const
     DARBS_TRY(reserve(ctx, ctx->depth_keys, sizeof(unsigned) * 2 * nn));
     DARBS_TRY(reserve(ctx, ctx->order, sizeof(unsigned) * 2 * nn));
     DARBS_TRY(reserve(ctx, ctx->offsets, sizeof(unsigned) * (nn + 1)));
+    if (sinks) {
+        sinks->rects = (uint2*)ctx->rects.ptr;
+        sinks->touched = (unsigned*)(sinks->rects + nn);
+        sinks->depth_keys = (unsigned*)ctx->depth_keys.ptr;
+        sinks->order = (unsigned*)ctx->order.ptr;
+        sinks->skipped_nonfinite = &scalars->skipped_nonfinite;
+        sinks->tiles_x = ctx->tiles_x;
+        sinks->tiles_y = ctx->tiles_y;
+    }
+    return DARBS_OK;
+}
+
+// rects_done: a fused preprocess already filled the sinks of binning_begin (which the caller ran).
+darbs_status run_binning(darbs_cuda_ctx* ctx, int64_t n, const float* mu2, const float* conic,
+                         const float* radius, const float* depth, const int32_t* valid,
+                         int width, int height, bool rects_done) {
+    cudaStream_t s = ctx->stream;
+    if (!rects_done) DARBS_TRY(binning_begin(ctx, n, width, height, nullptr));
+    const int tiles = ctx->tiles_x * ctx->tiles_y;
+    if (n == 0 || tiles == 0) return DARBS_OK;
+    Scalars* scalars = (Scalars*)((unsigned long long*)ctx->counters.ptr + 8);
+    const size_t nn = (size_t)n;
     uint2* rects = (uint2*)ctx->rects.ptr;
     unsigned* touched = (unsigned*)(rects + nn);
     // double buffers are split at half of the RESERVED size so that the halves
@@ -231,9 +225,11 @@ darbs_status run_binning(darbs_cuda_ctx* ctx, int64_t n, const float* mu2, const
     unsigned* or1 = or0 + ctx->order.bytes / 8;
     unsigned* offsets = (unsigned*)ctx->offsets.ptr;
 
-    rect_kernel<<<grid_for(n, 256), 256, 0, s>>>(n, mu2, conic, radius, depth, valid, ctx->tiles_x,
-                                                 ctx->tiles_y, rects, touched, dk0, or0, scalars);
-    DARBS_TRY(check_launch(ctx, "rect_kernel"));
+    if (!rects_done) {
+        rect_kernel<<<grid_for(n, 256), 256, 0, s>>>(n, mu2, conic, radius, depth, valid, ctx->tiles_x,
+                                                     ctx->tiles_y, rects, touched, dk0, or0, scalars);
+        DARBS_TRY(check_launch(ctx, "rect_kernel"));
+    }
 
     // 1. stable depth sort
     cub::DoubleBuffer<unsigned> dkeys(dk0, dk1);

@@ -160,6 +160,18 @@ darbs_status check_launch(darbs_cuda_ctx* ctx, const char* what, int launches = 
 // host-side kernel validation shared by the ABI (kernel.cpp:42-65)
 darbs_status make_kparams(darbs_cuda_ctx* ctx, const darbs_kernel_spec* spec, KParams* out);
 
+// Where the fused preprocess leaves what binning and the render kernels need (all null when the
+// stages run separately).
+struct SplatSinks {
+    float4* recs = nullptr;           // n x kRecVecs
+    uint2* rects = nullptr;           // n
+    unsigned* touched = nullptr;      // n
+    unsigned* depth_keys = nullptr;   // n
+    unsigned* order = nullptr;        // n
+    unsigned long long* skipped_nonfinite = nullptr;
+    int tiles_x = 0, tiles_y = 0;
+};
+
 // ---------------------------------------------------------------- launchers
 // render.cu
 darbs_status launch_pack(darbs_cuda_ctx* ctx, const KParams& kp, int64_t n, const float* mu2,
@@ -179,9 +191,10 @@ darbs_status launch_sum_counts(darbs_cuda_ctx* ctx, int64_t px, const int32_t* p
                                const int32_t* contributors);
 
 // binning.cu
+darbs_status binning_begin(darbs_cuda_ctx* ctx, int64_t n, int width, int height, SplatSinks* sinks);
 darbs_status run_binning(darbs_cuda_ctx* ctx, int64_t n, const float* mu2, const float* conic,
                          const float* radius, const float* depth, const int32_t* valid,
-                         int width, int height);
+                         int width, int height, bool rects_done = false);
 darbs_status export_bins(darbs_cuda_ctx* ctx, int64_t n, int32_t* tile_ranges, int32_t* point_list,
                          uint64_t* sort_keys, int32_t* depth_order);
 const int32_t* point_list_ptr(const darbs_cuda_ctx* ctx);
@@ -198,7 +211,8 @@ darbs_status launch_realize(darbs_cuda_ctx* ctx, int64_t n, const float* raw, fl
 darbs_status launch_project(darbs_cuda_ctx* ctx, const KParams& kp, double psi, double dilation,
                             int64_t n, const float* params, bool raw, const CameraD& cam,
                             int32_t* valid, float* mu2, float* cov2, float* conic, float* radius,
-                            float* depth, float* opacity, float* rgb, int* status_flags);
+                            float* depth, float* opacity, float* rgb, int* status_flags,
+                            const SplatSinks* sinks = nullptr);
 darbs_status launch_backward_projection(darbs_cuda_ctx* ctx, double psi, int64_t n,
                                         const float* grad_cov2, const float* grad_mu2,
                                         const float* prims, const CameraD& cam, float* d_mu,

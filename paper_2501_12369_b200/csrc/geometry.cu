@@ -15,7 +15,7 @@
 // stored results are rounded to float32.  That keeps the integer-valued radius
 // (ceil, geometry.cpp:62) and the near-plane test on the values the FP64
 // reference sees.
-#include "family.cuh"
+#include "splat.cuh"
 
 namespace darbs_b200 {
 
@@ -177,7 +177,7 @@ __global__ void project_kernel(KParams kp, double psi, double dilation, int64_t 
                                float* __restrict__ cov2, float* __restrict__ conic,
                                float* __restrict__ radius, float* __restrict__ depth,
                                float* __restrict__ opacity, float* __restrict__ rgb,
-                               int* __restrict__ flags) {
+                               int* __restrict__ flags, SplatSinks sinks) {
     int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     const bool in = i < n;
     const CameraT<double> cam(cam_d);
@@ -235,6 +235,20 @@ __global__ void project_kernel(KParams kp, double psi, double dilation, int64_t 
         rgb[3 * i] = (float)p.col[0];
         rgb[3 * i + 1] = (float)p.col[1];
         rgb[3 * i + 2] = (float)p.col[2];
+    }
+    // training step: what rect_kernel and pack_kernel would derive from the arrays just written
+    // (same float32 values in, same bits out), without a second and third pass over them
+    if (sinks.recs) {
+        uint2 rect;
+        unsigned cnt;
+        splat_rect(vis, o_mu[0], o_mu[1], o_con[0], o_con[1], o_con[2], o_rad, sinks.tiles_x, sinks.tiles_y,
+                   sinks.skipped_nonfinite, rect, cnt);
+        sinks.rects[i] = rect;
+        sinks.touched[i] = cnt;
+        sinks.depth_keys[i] = depth_to_key(o_dep);
+        sinks.order[i] = (unsigned)i;
+        splat_record(kp, o_mu[0], o_mu[1], o_con[0], o_con[1], o_con[2], (float)p.o, (float)p.col[0],
+                     (float)p.col[1], (float)p.col[2], sinks.recs + kRecVecs * i);
     }
 }
 
@@ -492,11 +506,13 @@ darbs_status launch_realize(darbs_cuda_ctx* ctx, int64_t n, const float* raw, fl
 darbs_status launch_project(darbs_cuda_ctx* ctx, const KParams& kp, double psi, double dilation,
                             int64_t n, const float* params, bool raw, const CameraD& cam,
                             int32_t* valid, float* mu2, float* cov2, float* conic, float* radius,
-                            float* depth, float* opacity, float* rgb, int* status_flags) {
+                            float* depth, float* opacity, float* rgb, int* status_flags,
+                            const SplatSinks* sinks) {
     if (n == 0) return DARBS_OK;
     project_kernel<<<grid_for(n, 128), 128, 0, ctx->stream>>>(kp, psi, dilation, n, params, raw, cam,
                                                              valid, mu2, cov2, conic, radius, depth,
-                                                             opacity, rgb, status_flags);
+                                                             opacity, rgb, status_flags,
+                                                             sinks ? *sinks : SplatSinks());
     return check_launch(ctx, "project_kernel");
 }
 

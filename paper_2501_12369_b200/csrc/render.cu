@@ -29,7 +29,7 @@
 // against a per-splat precomputed boundary; when the FP32 value lies inside a guard
 // band of that boundary the decision is re-taken in FP64 with the reference's own
 // expression order, so integer outputs match the FP64 reference.
-#include "family.cuh"
+#include "splat.cuh"
 
 namespace darbs_b200 {
 
@@ -51,21 +51,8 @@ __global__ void pack_kernel(KParams kp, int64_t n, const float* __restrict__ mu2
                             const float* __restrict__ rgb, float4* __restrict__ recs) {
     int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i >= n) return;
-    float mx = mu2[2 * i], my = mu2[2 * i + 1];
-    float a = conic[3 * i], b = conic[3 * i + 1], c = conic[3 * i + 2];
-    float o = opacity[i];
-    double ad = a, bd = b, cd = c;
-    double thr = family_threshold(kp, (double)o);
-    // An indefinite or non-finite conic cannot be culled by the convex block
-    // test and may produce dm2 < 0 (rasterizer.cpp:91): force the FP64 path.
-    bool pd = (ad > 0.0) && (cd > 0.0) && (ad * cd - bd * bd > 0.0);
-    float thr_m = pd ? (float)(thr * (double)kp.scale) : __int_as_float(0x7fc00000);
-    float4* r = recs + kRecVecs * i;
-    r[0] = make_float4(mx, my, kp.scale * a, kp.scale * (2.0f * b));
-    // cull helpers: minimiser slope along the other axis, -B/(2C) and -B/(2A)
-    r[1] = make_float4(kp.scale * c, o, thr_m, -b / c);
-    r[2] = make_float4(rgb[3 * i], rgb[3 * i + 1], rgb[3 * i + 2], -b / a);
-    r[3] = make_float4(a, b, c, 0.f);
+    splat_record(kp, mu2[2 * i], mu2[2 * i + 1], conic[3 * i], conic[3 * i + 1], conic[3 * i + 2], opacity[i],
+                 rgb[3 * i], rgb[3 * i + 1], rgb[3 * i + 2], recs + kRecVecs * i);
 }
 
 // ------------------------------------------------------------ shared pieces
