@@ -5,9 +5,11 @@
 // Two-level sort instead of one wide (tile, depth) key:
 //   1. stable LSD radix sort of the N (depth bits, index) pairs  -> depth order
 //      (stability gives the reference's index tie-break, rasterizer.cpp:33);
-//   2. tiles touched per splat, scanned IN DEPTH ORDER -> write offsets;
+//   2. tiles touched per splat, scanned IN DEPTH ORDER (read through the order by an input
+//      iterator of the scan) -> write offsets;
 //   3. every splat emits its (tile id, index) pairs at its offset, so the K
-//      entries are already depth-ordered globally;
+//      entries are already depth-ordered globally (a warp writes the entries of its 32
+//      splats as one contiguous run);
 //   4. stable radix sort of the K entries on the tile id bits only
 //      (13 bits at 1080p: two 7-bit... passes) keeps depth order inside a tile;
 //   5. tile ranges from the sorted tile ids.
@@ -15,6 +17,8 @@
 // floor((mu -+ R)/16) is decided on exactly the values the FP64 reference sees
 // (rasterizer.cpp:40-45).
 #include <cub/cub.cuh>
+#include <thrust/iterator/counting_iterator.h>
+#include <thrust/iterator/transform_iterator.h>
 
 #include "splat.cuh"
 
@@ -45,21 +49,22 @@ __global__ void rect_kernel(int64_t n, const float* __restrict__ mu2,
     touched[i] = cnt;
 }
 
-// touched[] gathered through the depth order, so the scan runs in depth order.
-__global__ void gather_touched_kernel(int64_t n, const unsigned* __restrict__ touched,
-                                      const unsigned* __restrict__ order,
-                                      unsigned* __restrict__ touched_in_order) {
-    int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (r < n) touched_in_order[r] = touched[order[r]];
-}
+// touched[] read through the depth order, so that the scan runs in depth order without a
+// gathered copy of the counts (an input iterator of the scan).
+struct TouchedInOrder {
+    const unsigned* touched;
+    const unsigned* order;
+    __host__ __device__ unsigned operator()(unsigned r) const { return touched[order[r]]; }
+};
+using TouchedIter = thrust::transform_iterator<TouchedInOrder, thrust::counting_iterator<unsigned>>;
 
 // K goes both to the device scalars and straight into pinned host memory (mapped under UVA): the
 // host needs it to size the tile sort, and a write from the SM does not queue behind a bulk
 // host <-> device copy that may be in flight on the copy engines.
 __global__ void total_kernel(int64_t n, const unsigned* __restrict__ offsets,
-                             const unsigned* __restrict__ touched_in_order,
+                             const unsigned* __restrict__ touched, const unsigned* __restrict__ order,
                              Scalars* __restrict__ scalars, volatile unsigned long long* host_total) {
-    const unsigned long long k = (unsigned long long)offsets[n - 1] + touched_in_order[n - 1];
+    const unsigned long long k = (unsigned long long)offsets[n - 1] + touched[order[n - 1]];
     scalars->total_entries = k;
     *host_total = k;
     __threadfence_system();
@@ -68,34 +73,72 @@ __global__ void total_kernel(int64_t n, const unsigned* __restrict__ offsets,
 // TileKey: unsigned short while the tile ids fit 16 bits (every size of BASELINE.json does; 4K has
 // 32 400 tiles), unsigned otherwise.  The tile sort then moves 6 bytes per entry and pass, not 8.
 template <typename TileKey>
-__global__ void duplicate_kernel(int64_t n, const unsigned* __restrict__ order,
-                                 const unsigned* __restrict__ offsets,
-                                 const uint2* __restrict__ rects,
-                                 const unsigned* __restrict__ touched, int tiles_x,
-                                 TileKey* __restrict__ tile_keys, unsigned* __restrict__ tile_vals) {
-    int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (r >= n) return;
-    unsigned idx = order[r];
-    uint2 rect = rects[idx];
-    int x0 = rect.x & 0xffff, y0 = rect.x >> 16, x1 = rect.y & 0xffff, y1 = rect.y >> 16;
-    unsigned off = offsets[r];
-    if (touched[idx] == 0) return;  // empty rect is stored as (0,0)-(0,0)
-    for (int ty = y0; ty <= y1; ++ty)
-        for (int tx = x0; tx <= x1; ++tx) {  // rasterizer.cpp:46-50
-            tile_keys[off] = (TileKey)(ty * tiles_x + tx);
-            tile_vals[off] = idx;
-            ++off;
+__global__ void __launch_bounds__(256)
+duplicate_kernel(int64_t n, const unsigned* __restrict__ order, const unsigned* __restrict__ offsets,
+                 const uint2* __restrict__ rects, const unsigned* __restrict__ touched, int tiles_x,
+                 TileKey* __restrict__ tile_keys, unsigned* __restrict__ tile_vals) {
+    // A warp takes 32 consecutive depth ranks and writes their entries TOGETHER: lane l owns the
+    // splat of rank r0 + l, but entry e of the warp's run is written by lane e mod 32, which
+    // finds the owning splat by a binary search over the lanes' offsets.  The writes of a warp
+    // are then one contiguous run instead of 32 interleaved short ones (rasterizer.cpp:46-50).
+    const unsigned full = 0xffffffffu;
+    const int lane = threadIdx.x & 31;
+    const int64_t r0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) - lane;
+    if (r0 >= n) return;
+    const int64_t r = r0 + lane;
+    unsigned idx = 0, cnt = 0, off = 0;
+    uint2 rect = make_uint2(0, 0);
+    if (r < n) {
+        idx = order[r];
+        rect = rects[idx];
+        cnt = touched[idx];
+        off = offsets[r];
+    }
+    const unsigned base = __shfl_sync(full, off, 0);
+    // lanes past n inherit the end of the run, so that the search never lands on them
+    const int last = (int)min((int64_t)31, n - 1 - r0);
+    const unsigned end = __shfl_sync(full, off + cnt, last);
+    const unsigned rel = (r < n ? off : end) - base;
+    const unsigned total = end - base;
+    for (unsigned e0 = 0; e0 < total; e0 += 32) {  // warp-uniform trip count: the shuffles need every lane
+        const unsigned e = e0 + lane;
+        int lo = 0;  // largest lane whose offset is <= e (zero-count lanes share the offset of the next)
+#pragma unroll
+        for (int step = 16; step > 0; step >>= 1) {
+            const unsigned probe = __shfl_sync(full, rel, min(lo + step, 31));
+            if (lo + step <= 31 && probe <= e) lo += step;
         }
+        const unsigned o_rel = __shfl_sync(full, rel, lo);
+        const unsigned o_idx = __shfl_sync(full, idx, lo);
+        const unsigned rx = __shfl_sync(full, rect.x, lo), ry = __shfl_sync(full, rect.y, lo);
+        const unsigned x0 = rx & 0xffff, y0 = rx >> 16, w = (ry & 0xffff) - x0 + 1;
+        if (e < total) {
+            const unsigned q = e - o_rel;
+            const unsigned qy = q / w, qx = q - qy * w;
+            tile_keys[base + e] = (TileKey)((y0 + qy) * tiles_x + x0 + qx);
+            tile_vals[base + e] = o_idx;
+        }
+    }
 }
 
 template <typename TileKey>
 __global__ void ranges_kernel(int64_t k, const TileKey* __restrict__ sorted_tiles,
                               int2* __restrict__ ranges) {
-    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (i >= k) return;
-    unsigned t = sorted_tiles[i];
-    if (i == 0 || sorted_tiles[i - 1] != t) ranges[t].x = (int)i;
-    if (i == k - 1 || sorted_tiles[i + 1] != t) ranges[t].y = (int)(i + 1);
+    // eight consecutive entries per thread: one boundary test per entry against its predecessor
+    constexpr int kPer = 8;
+    const int64_t first = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) * kPer;
+    if (first >= k) return;
+    unsigned prev = first > 0 ? (unsigned)sorted_tiles[first - 1] : 0xffffffffu;
+    const int64_t stop = first + kPer < k ? first + kPer : k;
+    for (int64_t i = first; i < stop; ++i) {
+        const unsigned t = sorted_tiles[i];
+        if (t != prev) {
+            ranges[t].x = (int)i;
+            if (prev != 0xffffffffu) ranges[prev].y = (int)i;
+        }
+        prev = t;
+    }
+    if (stop == k) ranges[prev].y = (int)k;
 }
 
 template <typename TileKey>
@@ -162,7 +205,7 @@ darbs_status tile_sort(darbs_cuda_ctx* ctx, int64_t n, int64_t k, int tiles, con
     const TileKey* sorted_tiles = tkeys.Current();
 
     // 5. ranges
-    ranges_kernel<TileKey><<<grid_for((int64_t)k, 256), 256, 0, s>>>((int64_t)k, sorted_tiles,
+    ranges_kernel<TileKey><<<grid_for(((int64_t)k + 7) / 8, 256), 256, 0, s>>>((int64_t)k, sorted_tiles,
                                                             (int2*)ctx->ranges.ptr);
     return check_launch(ctx, "ranges_kernel");
 }
@@ -238,7 +281,8 @@ darbs_status run_binning(darbs_cuda_ctx* ctx, int64_t n, const float* mu2, const
     DARBS_CUDA_TRY(ctx, cub::DeviceRadixSort::SortPairs(nullptr, temp_bytes, dkeys, dvals, (int)n, 0,
                                                        32, s));
     size_t scan_bytes = 0;
-    DARBS_CUDA_TRY(ctx, cub::DeviceScan::ExclusiveSum(nullptr, scan_bytes, offsets, offsets, (int)n, s));
+    DARBS_CUDA_TRY(ctx, cub::DeviceScan::ExclusiveSum(nullptr, scan_bytes, TouchedIter(thrust::counting_iterator<unsigned>(0u), TouchedInOrder{nullptr, nullptr}),
+                                                     offsets, (int)n, s));
     DARBS_TRY(reserve(ctx, ctx->cub_temp, temp_bytes > scan_bytes ? temp_bytes : scan_bytes));
     temp_bytes = ctx->cub_temp.bytes;
     DARBS_CUDA_TRY(ctx, cub::DeviceRadixSort::SortPairs(ctx->cub_temp.ptr, temp_bytes, dkeys, dvals,
@@ -248,16 +292,12 @@ darbs_status run_binning(darbs_cuda_ctx* ctx, int64_t n, const float* mu2, const
     ctx->cur_order_buf = order == or0 ? 0 : 1;
 
     // 2. offsets in depth order, total K
-    // the inactive half of the depth-key double buffer holds touched-in-depth-order
-    unsigned* touched_in_order = dkeys.Current() == dk0 ? dk1 : dk0;
-    gather_touched_kernel<<<grid_for(n, 256), 256, 0, s>>>(n, touched, order, touched_in_order);
-    DARBS_TRY(check_launch(ctx, "gather_touched_kernel"));
+    TouchedIter in_order(thrust::counting_iterator<unsigned>(0u), TouchedInOrder{touched, order});
     scan_bytes = ctx->cub_temp.bytes;
-    DARBS_CUDA_TRY(ctx, cub::DeviceScan::ExclusiveSum(ctx->cub_temp.ptr, scan_bytes, touched_in_order,
-                                                     offsets, (int)n, s));
+    DARBS_CUDA_TRY(ctx, cub::DeviceScan::ExclusiveSum(ctx->cub_temp.ptr, scan_bytes, in_order, offsets, (int)n, s));
     ctx->launches += 2;
     DARBS_TRY(reserve_pinned(ctx, 64));
-    total_kernel<<<1, 1, 0, s>>>(n, offsets, touched_in_order, scalars, (volatile unsigned long long*)ctx->pinned);
+    total_kernel<<<1, 1, 0, s>>>(n, offsets, touched, order, scalars, (volatile unsigned long long*)ctx->pinned);
     DARBS_TRY(check_launch(ctx, "total_kernel"));
     DARBS_CUDA_TRY(ctx, cudaStreamSynchronize(s));
     const unsigned long long k = *(volatile unsigned long long*)ctx->pinned;
