@@ -258,18 +258,19 @@ def run_ours(args):
     def iteration(name, e2e: bool):
         k, psi = kernels[name]
         s = state[name]
-        s["grads"].zero_()
+        # one view per GPU and iteration: the view OVERWRITES the gradient buffer (accumulate=False),
+        # which is fit3d.cpp:107's fill followed by the first "+=" without a pass that zeroes 14 N floats
         if e2e:
             # the view's target image comes from pinned host memory through the C ABI
             # (image_space = DARBS_HOST); the loss of every iteration is read back to the host, one
             # iteration late (darbs_cuda_pop_loss) so that the read-back never drains the stream
             loss = ctx.evaluate_view(k, psi, s["params"], cam, bg, target=s["target_np"], lam=LAMBDA,
-                                     param_grads=s["grads"], want_loss=False)
+                                     param_grads=s["grads"], want_loss=False, accumulate=False)
             # the next iteration's target starts its upload under this iteration's render kernels
             ctx.prefetch_target(state[KERNELS[(KERNELS.index(name) + 1) % len(KERNELS)]]["target_np"])
         else:
             loss = ctx.evaluate_view(k, psi, s["params"], cam, bg, target=s["target"], lam=LAMBDA,
-                                     param_grads=s["grads"], want_loss=False)
+                                     param_grads=s["grads"], want_loss=False, accumulate=False)
         if world > 1:
             dist.all_reduce(s["grads"], op=dist.ReduceOp.SUM)  # gradients are summed over views, fit3d.cpp:148-158
         s["t"] += 1
@@ -352,8 +353,8 @@ def run_ours(args):
         acc = None
         reps = 3
         for _ in range(reps):
-            s["grads"].zero_()
-            ctx.evaluate_view(k, psi, s["params"], cam, bg, target=s["target"], lam=LAMBDA, param_grads=s["grads"])
+            ctx.evaluate_view(k, psi, s["params"], cam, bg, target=s["target"], lam=LAMBDA, param_grads=s["grads"],
+                              accumulate=False)
             st = ctx.stage_times()
             ctx.adam_step(s["params"].view(-1), s["grads"].view(-1), s["m"], s["v"], lrs, s["t"] + 1)
             st["adam"] = ctx.stage_times()["adam"]

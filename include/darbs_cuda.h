@@ -240,6 +240,12 @@ DARBS_API darbs_status darbs_cuda_evaluate_view(darbs_cuda_ctx* ctx,
                                                 darbs_space param_space,
                                                 darbs_space image_space);
 
+/* param_grads of darbs_cuda_evaluate_view: 1 (default) adds the view's gradients to what the
+ * array holds (fit3d.cpp:148-158); 0 makes the NEXT evaluate_view overwrite it, which is the
+ * reference's std::fill(grads, 0) (fit3d.cpp:107) followed by the first view's "+=" without the
+ * pass over the array that zeroes it.  The setting returns to 1 after that call. */
+DARBS_API darbs_status darbs_cuda_set_accumulate(darbs_cuda_ctx* ctx, int accumulate);
+
 /* Starts the upload of a view's target image (host memory, pinned for a truly asynchronous copy;
  * count = 3*w*h floats) ahead of the darbs_cuda_evaluate_view call that will pass the same
  * pointer as `target` with image_space = DARBS_HOST.  The transfer is queued on the context's

@@ -106,6 +106,7 @@ def _load():
     lib.darbs_cuda_upload.argtypes = [vp, vp, vp, C.c_uint64]
     lib.darbs_cuda_download.argtypes = [vp, vp, vp, C.c_uint64]
     lib.darbs_cuda_device_zero.argtypes = [vp, vp, C.c_uint64]
+    lib.darbs_cuda_set_accumulate.argtypes = [vp, i32]
     lib.darbs_cuda_set_stage_timing.argtypes = [vp, i32]
     lib.darbs_cuda_stage_times.argtypes = [vp, C.POINTER(dbl)]
     lib.darbs_cuda_work_counters.argtypes = [vp, C.POINTER(i64)]
@@ -121,7 +122,7 @@ EXPORTED_SYMBOLS = (
     "darbs_cuda_backward darbs_cuda_realize darbs_cuda_project darbs_cuda_backward_projection "
     "darbs_cuda_evaluate_view darbs_cuda_prefetch_target darbs_cuda_pop_loss darbs_cuda_adam_step darbs_cuda_set_stage_timing darbs_cuda_stage_times "
     "darbs_cuda_work_counters darbs_cuda_microbench darbs_cuda_loss_total darbs_cuda_device_alloc "
-    "darbs_cuda_device_free darbs_cuda_upload darbs_cuda_download darbs_cuda_device_zero"
+    "darbs_cuda_device_free darbs_cuda_upload darbs_cuda_download darbs_cuda_device_zero darbs_cuda_set_accumulate"
 ).split()
 
 
@@ -423,8 +424,12 @@ class Context:
     # ------------------------------------------------------------ training
     def evaluate_view(self, kernel: KernelSpec, psi: float, raw_params, camera, background=(0.0, 0.0, 0.0),
                       target=None, lam: float = 0.0, grad_image=None, param_grads=None, image_out=None,
-                      want_loss: bool = True):
-        """One view of fit_scene's evaluate, src/fit3d.cpp:108-159.  Returns (total, l1, dssim, mse)."""
+                      want_loss: bool = True, accumulate: bool = True):
+        """One view of fit_scene's evaluate, src/fit3d.cpp:108-159.  Returns (total, l1, dssim, mse).
+        accumulate=False overwrites param_grads instead of adding to it (the first view of an
+        iteration: fit3d.cpp:107's fill without the pass that zeroes the array)."""
+        if not accumulate:
+            self._check(_lib.darbs_cuda_set_accumulate(self._h, 0))
         a, ai = _Args(), _Args()  # parameters and images may live in different spaces
         n = (raw_params.numel() if _is_torch(raw_params) else np.asarray(raw_params).size) // 14
         cam, pcam = _cam(camera)

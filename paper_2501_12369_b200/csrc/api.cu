@@ -785,7 +785,12 @@ darbs_status darbs_cuda_evaluate_view(darbs_cuda_ctx* ctx, const darbs_kernel_sp
         DARBS_TRY(sti.in_late(target, 3 * px, &d_target));  // not needed before the loss: overlaps the forward
     }
     DARBS_TRY(sti.in(grad_image, 3 * px, &d_gimg));
-    DARBS_TRY(st.inout(param_grads, 14 * nn, &d_pgrads));
+    const bool overwrite = !ctx->accumulate;
+    ctx->accumulate = 1;
+    if (overwrite)
+        DARBS_TRY(st.out(param_grads, 14 * nn, &d_pgrads));
+    else
+        DARBS_TRY(st.inout(param_grads, 14 * nn, &d_pgrads));
     DARBS_TRY(sti.out(image_out, 3 * px, &d_image));
 
     // internal SoA of the projected splats (one slot each; no compaction)
@@ -838,7 +843,7 @@ darbs_status darbs_cuda_evaluate_view(darbs_cuda_ctx* ctx, const darbs_kernel_sp
         {
             StageScope ts(ctx, ST_PREPROCESS_BWD);
             DARBS_TRY(launch_param_grads(ctx, psi, n, d_raw, cam, d_valid, (const float*)ctx->splat_grads.ptr,
-                                         d_conic, d_pgrads));
+                                         d_conic, d_pgrads, overwrite));
         }
     }
     DARBS_TRY(st.finish());
@@ -862,6 +867,12 @@ darbs_status darbs_cuda_evaluate_view(darbs_cuda_ctx* ctx, const darbs_kernel_sp
         while (ctx->loss_pending > 0) st_last = darbs_cuda_pop_loss(ctx, loss_out);
         return st_last;
     }
+    return DARBS_OK;
+}
+
+darbs_status darbs_cuda_set_accumulate(darbs_cuda_ctx* ctx, int accumulate) {
+    CTX_OR_FAIL(ctx);
+    ctx->accumulate = accumulate ? 1 : 0;
     return DARBS_OK;
 }
 

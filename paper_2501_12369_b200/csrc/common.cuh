@@ -85,6 +85,7 @@ struct darbs_cuda_ctx {
     int64_t launches = 0;
     int exact = 1;
     int timing = 0;
+    int accumulate = 1;  // evaluate_view adds to param_grads (0: the next call overwrites)
     double stage_ms[8] = {0, 0, 0, 0, 0, 0, 0, 0};
 
     // grow-only device workspace
@@ -219,7 +220,7 @@ darbs_status launch_backward_projection(darbs_cuda_ctx* ctx, double psi, int64_t
                                         float* d_scale, float* d_rot);
 darbs_status launch_param_grads(darbs_cuda_ctx* ctx, double psi, int64_t n, const float* raw,
                                 const CameraD& cam, const int32_t* valid, const float* splat_grads,
-                                const float* conic, float* param_grads);
+                                const float* conic, float* param_grads, bool overwrite);
 darbs_status launch_adam(darbs_cuda_ctx* ctx, int64_t dim, float* params, const float* grads,
                          float* m, float* v, const float* lrs, int t);
 darbs_status launch_l1_loss(darbs_cuda_ctx* ctx, int64_t count, const float* image,

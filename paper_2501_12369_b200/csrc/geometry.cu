@@ -376,17 +376,26 @@ __global__ void backward_projection_kernel(double psi, int64_t n, const float* _
 __global__ void __launch_bounds__(128)
 param_grads_kernel(double psi_d, int64_t n, const float* __restrict__ raw, CameraD cam_d,
                    const int* __restrict__ valid, const float* __restrict__ splat_grads,
-                   float* __restrict__ param_grads) {
+                   float* __restrict__ param_grads, bool overwrite) {
     using T = float;
     int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i >= n) return;
-    if (!valid[i]) return;
+    float2* g = reinterpret_cast<float2*>(param_grads + 14 * i);
+    if (!valid[i]) {  // culled in this view: adds nothing (and is cleared when this view overwrites)
+        if (overwrite)
+            for (int k = 0; k < 7; ++k) g[k] = make_float2(0.f, 0.f);
+        return;
+    }
     const CameraT<T> cam(cam_d);
     const T psi = (T)psi_d;
     PrimT<T> p;
     load_prim(raw + 14 * i, true, p);
     ProjectedT<T> pr;
-    if (!project_core(p, cam, psi, (T)DARBS_DILATION, pr)) return;
+    if (!project_core(p, cam, psi, (T)DARBS_DILATION, pr)) {
+        if (overwrite)
+            for (int k = 0; k < 7; ++k) g[k] = make_float2(0.f, 0.f);
+        return;
+    }
     // padded rows, SplatGrads order in the first nine
     const float4* gi4 = reinterpret_cast<const float4*>(splat_grads + kSplatGradRow * i);
     const float4 g0 = __ldg(gi4), g1 = __ldg(gi4 + 1);
@@ -403,13 +412,12 @@ param_grads_kernel(double psi_d, int64_t n, const float* __restrict__ raw, Camer
     T dm[3], ds[3], dq[4];
     backward_projection_core(p, cam, pr, psi, dcov, gm, dm, ds, dq);
     // fit3d.cpp:148-158: grads[owner] += ..., 14 floats per primitive as seven 64-bit read-modify-writes
-    float2* g = reinterpret_cast<float2*>(param_grads + 14 * i);
     const float add[14] = {dm[0], dm[1], dm[2], ds[0] * p.s[0], ds[1] * p.s[1], ds[2] * p.s[2], dq[0], dq[1],
                            dq[2], dq[3], g0.w * p.o * (1.0f - p.o), g0.x * p.col[0] * (1.0f - p.col[0]),
                            g0.y * p.col[1] * (1.0f - p.col[1]), g0.z * p.col[2] * (1.0f - p.col[2])};
 #pragma unroll
     for (int k = 0; k < 7; ++k) {
-        float2 v = g[k];
+        float2 v = overwrite ? make_float2(0.f, 0.f) : g[k];
         v.x += add[2 * k];
         v.y += add[2 * k + 1];
         g[k] = v;
@@ -528,10 +536,10 @@ darbs_status launch_backward_projection(darbs_cuda_ctx* ctx, double psi, int64_t
 
 darbs_status launch_param_grads(darbs_cuda_ctx* ctx, double psi, int64_t n, const float* raw,
                                 const CameraD& cam, const int32_t* valid, const float* splat_grads,
-                                const float* /*conic*/, float* param_grads) {
+                                const float* /*conic*/, float* param_grads, bool overwrite) {
     if (n == 0) return DARBS_OK;
     param_grads_kernel<<<grid_for(n, 128), 128, 0, ctx->stream>>>(psi, n, raw, cam, valid, splat_grads,
-                                                                 param_grads);
+                                                                 param_grads, overwrite);
     return check_launch(ctx, "param_grads_kernel");
 }
 

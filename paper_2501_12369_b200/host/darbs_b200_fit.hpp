@@ -570,7 +570,6 @@ inline Fit3DResult fit_scene(const std::vector<View>& views, const KernelSpec& k
     // one evaluation over all views (fit3d.cpp:104-167); losses are collected one view late
     auto evaluate = [&](bool with_grad) {
         IterStats s;
-        if (with_grad) d_grads.zero();
         std::size_t popped = 0;
         auto pop = [&] {
             double out[4];
@@ -582,6 +581,8 @@ inline Fit3DResult fit_scene(const std::vector<View>& views, const KernelSpec& k
             ++popped;
         };
         for (std::size_t v = 0; v < views.size(); ++v) {
+            // the first view overwrites the gradient buffer: fit3d.cpp:107's fill without a zeroing pass
+            if (with_grad && v == 0) throw_status(darbs_cuda_set_accumulate(ctx, 0), ctx);
             throw_status(darbs_cuda_evaluate_view(ctx, &ks, psi, (int64_t)n, d_params.data(), blocks[v].data(), bg,
                                                   d_targets[v].data(), config.lambda, nullptr,
                                                   with_grad ? d_grads.data() : nullptr, nullptr, nullptr,

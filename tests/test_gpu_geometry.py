@@ -195,6 +195,26 @@ def test_evaluate_view_matches_oracle_chain(ctx, port, darbs, name):
     assert rel_err(pg2, 2.0 * pg.astype(np.float64), 1e-4 * max(1.0, np.abs(ref).max())).max() <= 1e-3
 
 
+def test_evaluate_view_overwrite_mode(ctx, darbs):
+    """accumulate=False: the view overwrites param_grads (zeros for culled primitives), exactly
+    what a zero fill followed by "+=" gives (fit3d.cpp:107, :148-158)."""
+    gk = darbs.kernel_preset("raised-cosine")
+    psi = darbs.default_psi("raised-cosine")
+    n, w, h = 300, 64, 64
+    raw = random_raw(n, 8)
+    raw[7, 0:3] = (3.5288, 1.1492, 1.4920)  # behind the demo camera
+    gimg = f32(np.random.default_rng(3).normal(size=(h, w, 3)))
+    ref = np.zeros((n, 14), np.float32)
+    ctx.evaluate_view(gk, psi, raw, DEMO_CAMERA, (0, 0, 0), grad_image=gimg, param_grads=ref)
+    got = np.full((n, 14), 7.0, np.float32)  # stale contents must not survive
+    ctx.evaluate_view(gk, psi, raw, DEMO_CAMERA, (0, 0, 0), grad_image=gimg, param_grads=got, accumulate=False)
+    assert np.all(got[7] == 0.0)
+    assert rel_err(got, ref, 1e-4 * max(1.0, np.abs(ref).max())).max() <= 1e-3
+    # the setting applies to one call only: the next one accumulates again
+    ctx.evaluate_view(gk, psi, raw, DEMO_CAMERA, (0, 0, 0), grad_image=gimg, param_grads=got)
+    assert rel_err(got, 2.0 * ref.astype(np.float64), 1e-4 * max(1.0, np.abs(ref).max())).max() <= 1e-3
+
+
 def test_evaluate_view_l1_loss_and_errors(ctx, port, darbs):
     """L1 branch of loss_total (loss.cpp:183-188, lambda = 0) and the two numeric_error exits of
     evaluate (fit3d.cpp:117-119)."""
