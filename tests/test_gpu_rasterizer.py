@@ -73,6 +73,16 @@ def test_bins_bit_exact(ctx, port, name, shape, seed):
     check_bins(ctx, port, s, w, h)
 
 
+def test_bins_more_than_65536_tiles(ctx, port):
+    """Beyond 65 536 tiles the tile sort switches from 16-bit to 32-bit keys (4208 x 4208 pixels =
+    263 x 263 tiles); a few splats are made huge so that lists cross many tiles."""
+    k = port.preset("gaussian")
+    w = h = 4208
+    s = port.random_scene(k, 3000, w, h, 5)
+    s.radius[:8] = 900.0
+    check_bins(ctx, port, s, w, h)
+
+
 def test_bins_equal_depth_index_order(ctx, port):
     """Equal depths are ordered by splat index, test_rasterizer.cpp:84-94."""
     k = port.preset("gaussian")
