@@ -340,14 +340,15 @@ darbs_status darbs_cuda_create(int device, darbs_cuda_ctx** out_ctx) {
     for (int i = 0; i < 16; ++i) cudaEventCreate(&ctx->timer.ev[i]);
     ctx->timer.created = true;
     cudaEventCreateWithFlags(&ctx->after_cull, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&ctx->k_ready, cudaEventDisableTiming);
     for (int i = 0; i < 2; ++i) cudaEventCreateWithFlags(&ctx->target_done[i], cudaEventDisableTiming);
     for (int i = 0; i < kLossRing; ++i) {
         cudaMallocHost(&ctx->loss_ring[i].host, 64);
         cudaEventCreateWithFlags(&ctx->loss_ring[i].done, cudaEventDisableTiming);
     }
-    darbs_status st = reserve(ctx, ctx->counters, 256);
+    darbs_status st = reserve(ctx, ctx->counters, 1024);  // 32 scalar slots + kSlotsK partial sums of K
     if (st == DARBS_OK) st = reserve_pinned(ctx, 256);
-    if (st == DARBS_OK && cudaMemsetAsync(ctx->counters.ptr, 0, 256, ctx->stream) != cudaSuccess)
+    if (st == DARBS_OK && cudaMemsetAsync(ctx->counters.ptr, 0, 1024, ctx->stream) != cudaSuccess)
         st = DARBS_CUDA_ERROR;
     if (st != DARBS_OK) {
         g_create_error = ctx->last_error;
@@ -380,6 +381,7 @@ void darbs_cuda_destroy(darbs_cuda_ctx* ctx) {
         if (ctx->loss_ring[i].done) cudaEventDestroy(ctx->loss_ring[i].done);
     }
     if (ctx->after_cull) cudaEventDestroy(ctx->after_cull);
+    if (ctx->k_ready) cudaEventDestroy(ctx->k_ready);
     for (int i = 0; i < 2; ++i) {
         if (ctx->target_done[i]) cudaEventDestroy(ctx->target_done[i]);
         if (ctx->target_stage[i].ptr) cudaFree(ctx->target_stage[i].ptr);

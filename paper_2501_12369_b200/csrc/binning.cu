@@ -36,7 +36,8 @@ __global__ void rect_kernel(int64_t n, const float* __restrict__ mu2,
                             const float* __restrict__ depth, const int* __restrict__ valid,
                             int tiles_x, int tiles_y, uint2* __restrict__ rects,
                             unsigned* __restrict__ touched, unsigned* __restrict__ depth_keys,
-                            unsigned* __restrict__ order, Scalars* __restrict__ scalars) {
+                            unsigned* __restrict__ order, Scalars* __restrict__ scalars,
+                            unsigned long long* __restrict__ k_slots) {
     int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i >= n) return;
     depth_keys[i] = depth_to_key(depth[i]);
@@ -47,6 +48,7 @@ __global__ void rect_kernel(int64_t n, const float* __restrict__ mu2,
                conic[3 * i + 2], radius[i], tiles_x, tiles_y, &scalars->skipped_nonfinite, rect, cnt);
     rects[i] = rect;
     touched[i] = cnt;
+    accumulate_tile_count(cnt, k_slots);
 }
 
 // touched[] read through the depth order, so that the scan runs in depth order without a
@@ -58,17 +60,22 @@ struct TouchedInOrder {
 };
 using TouchedIter = thrust::transform_iterator<TouchedInOrder, thrust::counting_iterator<unsigned>>;
 
-// K goes both to the device scalars and straight into pinned host memory (mapped under UVA): the
-// host needs it to size the tile sort, and a write from the SM does not queue behind a bulk
-// host <-> device copy that may be in flight on the copy engines.
-__global__ void total_kernel(int64_t n, const unsigned* __restrict__ offsets,
-                             const unsigned* __restrict__ touched, const unsigned* __restrict__ order,
-                             Scalars* __restrict__ scalars, volatile unsigned long long* host_total) {
-    const unsigned long long k = (unsigned long long)offsets[n - 1] + touched[order[n - 1]];
-    scalars->total_entries = k;
-    *host_total = k;
-    __threadfence_system();
+// K, the total of the per-splat tile counts (accumulated over kSlotsK addresses by the kernel
+// that made the rectangles), goes to the device scalars and straight into pinned host memory
+// (mapped under UVA): the host needs it to size the tile sort, and a write from the SM does not
+// queue behind a bulk host <-> device copy that may be in flight on the copy engines.  It is
+// known before the depth sort starts, so the host reads it while the GPU sorts.
+__global__ void total_kernel(const unsigned long long* __restrict__ k_slots, Scalars* __restrict__ scalars,
+                             volatile unsigned long long* host_total) {
+    unsigned long long k = k_slots[threadIdx.x] + k_slots[threadIdx.x + 32];
+    for (int o = 16; o > 0; o >>= 1) k += __shfl_xor_sync(0xffffffffu, k, o);
+    if (threadIdx.x == 0) {
+        scalars->total_entries = k;
+        *host_total = k;
+        __threadfence_system();
+    }
 }
+static_assert(kSlotsK == 64, "total_kernel sums two slots per lane");
 
 // TileKey: unsigned short while the tile ids fit 16 bits (every size of BASELINE.json does; 4K has
 // 32 400 tiles), unsigned otherwise.  The tile sort then moves 6 bytes per entry and pass, not 8.
@@ -225,6 +232,8 @@ darbs_status binning_begin(darbs_cuda_ctx* ctx, int64_t n, int width, int height
     DARBS_CUDA_TRY(ctx, cudaMemsetAsync(ctx->ranges.ptr, 0, sizeof(int2) * (size_t)tiles, s));
     Scalars* scalars = (Scalars*)((unsigned long long*)ctx->counters.ptr + 8);
     DARBS_CUDA_TRY(ctx, cudaMemsetAsync(ctx->counters.ptr, 0, sizeof(unsigned long long) * 10, s));
+    unsigned long long* k_slots = (unsigned long long*)ctx->counters.ptr + kSlotsKBase;
+    DARBS_CUDA_TRY(ctx, cudaMemsetAsync(k_slots, 0, sizeof(unsigned long long) * kSlotsK, s));
     ctx->fwd_entries = 0;
     ctx->cur_key_buf = 0;
     ctx->cur_order_buf = 0;
@@ -242,6 +251,7 @@ darbs_status binning_begin(darbs_cuda_ctx* ctx, int64_t n, int width, int height
         sinks->depth_keys = (unsigned*)ctx->depth_keys.ptr;
         sinks->order = (unsigned*)ctx->order.ptr;
         sinks->skipped_nonfinite = &scalars->skipped_nonfinite;
+        sinks->k_slots = k_slots;
         sinks->tiles_x = ctx->tiles_x;
         sinks->tiles_y = ctx->tiles_y;
     }
@@ -270,9 +280,16 @@ darbs_status run_binning(darbs_cuda_ctx* ctx, int64_t n, const float* mu2, const
 
     if (!rects_done) {
         rect_kernel<<<grid_for(n, 256), 256, 0, s>>>(n, mu2, conic, radius, depth, valid, ctx->tiles_x,
-                                                     ctx->tiles_y, rects, touched, dk0, or0, scalars);
+                                                     ctx->tiles_y, rects, touched, dk0, or0, scalars,
+                                                     (unsigned long long*)ctx->counters.ptr + kSlotsKBase);
         DARBS_TRY(check_launch(ctx, "rect_kernel"));
     }
+    // K is complete: publish it now, and let the host pick it up while the depth sort runs
+    DARBS_TRY(reserve_pinned(ctx, 64));
+    total_kernel<<<1, 32, 0, s>>>((const unsigned long long*)ctx->counters.ptr + kSlotsKBase, scalars,
+                                  (volatile unsigned long long*)ctx->pinned);
+    DARBS_TRY(check_launch(ctx, "total_kernel"));
+    DARBS_CUDA_TRY(ctx, cudaEventRecord(ctx->k_ready, s));
 
     // 1. stable depth sort
     cub::DoubleBuffer<unsigned> dkeys(dk0, dk1);
@@ -296,10 +313,9 @@ darbs_status run_binning(darbs_cuda_ctx* ctx, int64_t n, const float* mu2, const
     scan_bytes = ctx->cub_temp.bytes;
     DARBS_CUDA_TRY(ctx, cub::DeviceScan::ExclusiveSum(ctx->cub_temp.ptr, scan_bytes, in_order, offsets, (int)n, s));
     ctx->launches += 2;
-    DARBS_TRY(reserve_pinned(ctx, 64));
-    total_kernel<<<1, 1, 0, s>>>(n, offsets, touched, order, scalars, (volatile unsigned long long*)ctx->pinned);
-    DARBS_TRY(check_launch(ctx, "total_kernel"));
-    DARBS_CUDA_TRY(ctx, cudaStreamSynchronize(s));
+    // the host waits for K only (published before the depth sort): the GPU still has the sort and
+    // the scan queued, so it does not idle while the rest of the iteration is being launched
+    DARBS_CUDA_TRY(ctx, cudaEventSynchronize(ctx->k_ready));
     const unsigned long long k = *(volatile unsigned long long*)ctx->pinned;
     if (k >= (1ull << 31)) return fail(ctx, DARBS_INVALID_PARAMETER, "more than 2^31 tile entries");
     ctx->fwd_entries = (int64_t)k;

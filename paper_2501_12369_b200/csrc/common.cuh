@@ -117,6 +117,7 @@ struct darbs_cuda_ctx {
     cudaEvent_t target_done[2] = {nullptr, nullptr};
     int target_next = 0;
     cudaEvent_t after_cull = nullptr;  // the last forward's long kernels start here
+    cudaEvent_t k_ready = nullptr;     // binning: the entry count K has reached pinned host memory
     bool have_after_cull = false;
 
     darbs_b200::LossSlot loss_ring[darbs_b200::kLossRing];
@@ -163,6 +164,9 @@ darbs_status make_kparams(darbs_cuda_ctx* ctx, const darbs_kernel_spec* spec, KP
 
 // Where the fused preprocess leaves what binning and the render kernels need (all null when the
 // stages run separately).
+static constexpr int kSlotsK = 64;       // K is accumulated over this many addresses, by block index
+static constexpr int kSlotsKBase = 32;   // their position in ctx->counters, in u64 units
+
 struct SplatSinks {
     float4* recs = nullptr;           // n x kRecVecs
     uint2* rects = nullptr;           // n
@@ -170,6 +174,7 @@ struct SplatSinks {
     unsigned* depth_keys = nullptr;   // n
     unsigned* order = nullptr;        // n
     unsigned long long* skipped_nonfinite = nullptr;
+    unsigned long long* k_slots = nullptr;  // kSlotsK partial sums of the tile counts (K = their total)
     int tiles_x = 0, tiles_y = 0;
 };
 

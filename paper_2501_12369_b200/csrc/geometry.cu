@@ -245,6 +245,7 @@ __global__ void project_kernel(KParams kp, double psi, double dilation, int64_t 
                    sinks.skipped_nonfinite, rect, cnt);
         sinks.rects[i] = rect;
         sinks.touched[i] = cnt;
+        accumulate_tile_count(cnt, sinks.k_slots);
         sinks.depth_keys[i] = depth_to_key(o_dep);
         sinks.order[i] = (unsigned)i;
         splat_record(kp, o_mu[0], o_mu[1], o_con[0], o_con[1], o_con[2], (float)p.o, (float)p.col[0],

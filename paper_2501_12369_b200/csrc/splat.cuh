@@ -45,6 +45,16 @@ __device__ __forceinline__ void splat_rect(bool ok, float mxf, float myf, float 
     }
 }
 
+// K = the total of the tile counts: one atomic per warp, spread over kSlotsK addresses so that
+// the ~8 k warps of a million splats do not serialise on one.  Every thread of the (possibly
+// partial) warp that is still running calls this.
+__device__ __forceinline__ void accumulate_tile_count(unsigned cnt, unsigned long long* k_slots) {
+    const unsigned active = __activemask();
+    const unsigned sum = __reduce_add_sync(active, cnt);
+    if ((threadIdx.x & 31) == __ffs(active) - 1 && sum)
+        atomicAdd(k_slots + (blockIdx.x & (kSlotsK - 1)), (unsigned long long)sum);
+}
+
 __device__ __forceinline__ void splat_record(const KParams& kp, float mx, float my, float a, float b, float c,
                                              float o, float cr, float cg, float cb, float4* __restrict__ r) {
     double ad = a, bd = b, cd = c;
