@@ -36,7 +36,7 @@ namespace darbs_b200 {
 namespace {
 
 constexpr int kBlocksPerTile = 8;  // 2 x 4 blocks of 8 x 4 pixels
-constexpr int kWarpsPerCta = 8;
+constexpr int kWarpsPerCta = 4;  // cull CTA: one tile, 128 list entries per step
 constexpr int kThreads = 32 * kWarpsPerCta;
 constexpr unsigned kFull = 0xffffffffu;
 
@@ -340,8 +340,8 @@ cull_kernel(KParams kp, const float4* __restrict__ recs, const int2* __restrict_
         atomicAdd(counters + CNT_SURVIVORS, (unsigned long long)run);
     }
     __syncthreads();
-    {
-        const int b = warp, n = total[b];
+    for (int b = warp; b < kBlocksPerTile; b += kWarpsPerCta) {
+        const int n = total[b];
         const int padded = (n + kPad - 1) & ~(kPad - 1);
         if (n + lane < padded) store_null_entry(tile_streams + kEntryVecs * ((size_t)b * cap + (size_t)(n + lane)));
     }
