@@ -139,8 +139,9 @@ __device__ __noinline__ float4 exact_decide(const KParams& kp, const float4* __r
 // distance, computed by the caller with a fixed FMA order shared by forward
 // and backward so that both passes take identical decisions.  `near` flags a
 // value inside the guard band of a threshold (re-decided in FP64 when
-// kp.exact); a_raw = opacity * weight, unclamped.
-template <int FAM, bool GRAD>
+// kp.exact); a_raw = opacity * weight, unclamped.  CLAMPBAND: also watch the band of the alpha
+// clamp (the backward's gate, rasterizer.cpp:202).
+template <int FAM, bool GRAD, bool CLAMPBAND = GRAD>
 __device__ __forceinline__ void fast_decide(const KParams& kp, float m, float thr, float o,
                                             bool& hit, bool& near, float& a_raw, float& w,
                                             float& dwdm) {
@@ -151,7 +152,7 @@ __device__ __forceinline__ void fast_decide(const KParams& kp, float m, float th
         generic_eval(kp, fmaxf(m, 0.f), w, dwdm);
         a_raw = o * w;
         near = near || !(fabsf(a_raw - kAlphaSkipF) > 2e-6f);
-        if (GRAD) near = near || !(fabsf(a_raw - kAlphaClampF) > 2e-6f);
+        if (CLAMPBAND) near = near || !(fabsf(a_raw - kAlphaClampF) > 2e-6f);
         hit = in_support && !(fminf(kAlphaClampF, a_raw) < kAlphaSkipF);
     } else {
         const float d = thr - m;
@@ -164,7 +165,7 @@ __device__ __forceinline__ void fast_decide(const KParams& kp, float m, float th
             dwdm = 0.f;
         }
         a_raw = o * w;
-        if (GRAD) near = near || !(fabsf(a_raw - kAlphaClampF) > 2e-6f);
+        if (CLAMPBAND) near = near || !(fabsf(a_raw - kAlphaClampF) > 2e-6f);
     }
 }
 
@@ -393,9 +394,13 @@ struct FwdPixel {
     float2 crg;  // red and green accumulate in one packed FMA
     float T, cb;
     float contrib;  // contributor count, kept in FP32 (exact below 2^24) so a hit costs one FADD
-    int proc;
+    int nlive;      // stream entries met while live: the last of them is the one that crossed the floor
     unsigned nexact;
 };
+
+// Opacity from which alpha = o * w can reach the 0.99 clamp (rasterizer.cpp:93); FP32 weights
+// exceed 1 by rounding only.  Groups without such an entry run a variant without the clamp.
+constexpr float kClampableF = 0.98f;
 
 // Front-to-back compositing of one queued survivor into this lane's pixel
 // (rasterizer.cpp:88-100).  Branch-free: a lane that does not take the splat
@@ -405,7 +410,7 @@ struct FwdPixel {
 // survivors: it only records in near_acc whether any FP32 value fell inside
 // the guard band of a threshold; the group is then replayed from the saved
 // pixel state with CAREFUL = true, which re-takes those decisions in FP64.
-template <int FAM, bool CAREFUL>
+template <int FAM, bool CAREFUL, bool CLAMP>
 __device__ __forceinline__ void fwd_visit(const KParams& kp, const float4* __restrict__ recs,
                                           const float4* __restrict__ qe, float fx, float fy,
                                           FwdPixel& px, bool& near_acc) {
@@ -420,7 +425,7 @@ __device__ __forceinline__ void fwd_visit(const KParams& kp, const float4* __res
     bool hit, near;
     float a_raw, w, dwdm;
     fast_decide<FAM, false>(kp, m, s1.z, s1.y, hit, near, a_raw, w, dwdm);
-    float alpha = fminf(kAlphaClampF, a_raw);
+    float alpha = CLAMP ? fminf(kAlphaClampF, a_raw) : a_raw;
     if constexpr (CAREFUL) {
         if (kp.exact && near && live && __float_as_int(s2.w) >= 0) {
             const float4 r = exact_decide(kp, recs, __float_as_int(s2.w), fx, fy);
@@ -437,11 +442,11 @@ __device__ __forceinline__ void fwd_visit(const KParams& kp, const float4* __res
     const float at = alpha * px.T;
     px.crg = __ffma2_rn(make_float2(s2.x, s2.y), make_float2(at, at), px.crg);
     px.cb = fmaf(s2.z, at, px.cb);
-    const float Tn = fmaf(-alpha, px.T, px.T);
     px.contrib += hitf;
-    // the step that crossed the floor (a live lane that does not take the splat keeps T)
-    if (live && Tn < kTFloorF) px.proc = __float_as_int(s1.w) + 1;
-    px.T = Tn;
+    // T never rises and a dead lane blends alpha = 0, so the entries a lane meets while live are a
+    // prefix of the stream and the last of them is the one that crossed the floor
+    if (live) ++px.nlive;
+    px.T = fmaf(-alpha, px.T, px.T);
 }
 
 // Warps of a forward CTA.  A warp owns one 8x4 block and leaves as soon as its 32 pixels have
@@ -478,7 +483,7 @@ render_fwd_kernel(KParams kp, const float4* __restrict__ recs, const int2* __res
     px.crg = make_float2(0.f, 0.f);
     px.cb = 0.f;
     px.contrib = 0.f;
-    px.proc = end - beg;
+    px.nlive = 0;
     px.nexact = 0;
 
     const float4* src = streams + kEntryVecs * stream_offset(tile, beg, end, warp);
@@ -506,15 +511,27 @@ render_fwd_kernel(KParams kp, const float4* __restrict__ recs, const int2* __res
         const float4* qc = stage0 + stage * kChunkVecs;
         const int rem = n - c * kChunk;
         const int ngroups = rem >= kChunk ? kChunk / kGroup : (rem + kGroup - 1) / kGroup;
+        // entry `lane` of the chunk: can its alpha reach the clamp?  (What lies beyond the padding
+        // is never composited; its bits only cover groups that do not run.)
+        const unsigned clampable =
+            FAM == FAM_GENERIC ? kFull : __ballot_sync(kFull, !(qc[lane * kEntryVecs + 1].y < kClampableF));
         for (int g = 0; g < ngroups; ++g) {
             const float4* qb = qc + g * (kGroup * kEntryVecs);
             const FwdPixel save = px;
             bool near_acc = false;
+            if ((clampable >> (g * kGroup)) & ((1u << kGroup) - 1u)) {
 #pragma unroll
-            for (int j = 0; j < kGroup; ++j) fwd_visit<FAM, false>(kp, recs, qb + j * 3, fx, fy, px, near_acc);
+                for (int j = 0; j < kGroup; ++j)
+                    fwd_visit<FAM, false, true>(kp, recs, qb + j * 3, fx, fy, px, near_acc);
+            } else {
+#pragma unroll
+                for (int j = 0; j < kGroup; ++j)
+                    fwd_visit<FAM, false, false>(kp, recs, qb + j * 3, fx, fy, px, near_acc);
+            }
             if (kp.exact && __any_sync(kFull, near_acc)) {  // a few groups per thousand
                 px = save;
-                for (int j = 0; j < kGroup; ++j) fwd_visit<FAM, true>(kp, recs, qb + j * 3, fx, fy, px, near_acc);
+                for (int j = 0; j < kGroup; ++j)
+                    fwd_visit<FAM, true, true>(kp, recs, qb + j * 3, fx, fy, px, near_acc);
             }
         }
         used += ngroups * kGroup;
@@ -546,10 +563,12 @@ render_fwd_kernel(KParams kp, const float4* __restrict__ recs, const int2* __res
     unsigned nfloor = 0;
     if (inside) {
         nfloor = fabsf(px.T - kTFloorF) < 2e-9f;
-        if (px.T < kTFloorF && px.proc > 0) {
-            const int idx = __ldg(point_list + beg + px.proc - 1);
-            const float4 v0 = __ldg(recs + kRecVecs * (int64_t)idx);
-            const float4 v1 = __ldg(recs + kRecVecs * (int64_t)idx + 1);
+        // processed (rasterizer.cpp:86,100): the whole list, or up to the entry that crossed the floor
+        int proc = end - beg;
+        if (px.T < kTFloorF && px.nlive > 0) {
+            const float4 v0 = __ldg(src + (size_t)(px.nlive - 1) * kEntryVecs);
+            const float4 v1 = __ldg(src + (size_t)(px.nlive - 1) * kEntryVecs + 1);
+            proc = __float_as_int(v1.w) + 1;
             bool hit, near;
             float a_raw, w, dwdm;
             fast_decide<FAM, false>(kp, quad_m(v0.z, v0.w, v1.x, fx - v0.x, fy - v0.y), v1.z, v1.y, hit, near,
@@ -562,7 +581,7 @@ render_fwd_kernel(KParams kp, const float4* __restrict__ recs, const int2* __res
         image[p * 3 + 1] = fmaf(bg1, px.T, px.crg.y);
         image[p * 3 + 2] = fmaf(bg2, px.T, px.cb);
         t_final[p] = px.T;
-        processed[p] = px.proc;
+        processed[p] = proc;
         contributors[p] = (int)px.contrib;
     }
     // instrumentation: one atomic per warp per counter
@@ -615,7 +634,7 @@ struct BwdExchange {
     static constexpr bool kPair = FAM != FAM_GAUSS2;
 };
 
-template <int FAM, bool CAREFUL>
+template <int FAM, bool CAREFUL, bool CLAMP>
 __device__ __forceinline__ void bwd_visit(const KParams& kp, const float4* __restrict__ recs,
                                           const float4* __restrict__ qe, float fx, float fy,
                                           BwdPixel& px, float* __restrict__ xw,
@@ -628,7 +647,37 @@ __device__ __forceinline__ void bwd_visit(const KParams& kp, const float4* __res
     const bool elig = __float_as_int(s1.w) < px.nproc;
     bool hit, near;
     float a_raw, w, dwdm;
-    fast_decide<FAM, true>(kp, m, s1.z, s1.y, hit, near, a_raw, w, dwdm);
+    fast_decide<FAM, true, CLAMP>(kp, m, s1.z, s1.y, hit, near, a_raw, w, dwdm);
+    if constexpr (!CLAMP) {
+        // No entry of the group can reach the alpha clamp (opacity < kClampableF): alpha = o w, the
+        // gradient always passes (rasterizer.cpp:202), and there is no clamp band to watch.
+        static_assert(!CAREFUL, "the replay runs the full form");
+        near_acc = near_acc || near;
+        hit = hit && elig;
+        float alpha;
+        if constexpr (!BwdExchange<FAM>::kPair) {
+            w = hit ? w : 0.f;  // zeroes alpha and the exchanged y = d_alpha w at once
+            alpha = s1.y * w;
+        } else {
+            alpha = hit ? a_raw : 0.f;
+        }
+        // rasterizer.cpp:189-213 with s = <g, accum_behind>
+        const float rc = rcp_approx(1.0f - alpha);
+        const float t_before = px.T * rc;
+        const float wgt = alpha * t_before;
+        const float gc = fmaf(px.g2, s2.z, fmaf(px.g1, s2.y, px.g0 * s2.x));
+        const float d_alpha = fmaf(t_before, gc, -(rc * px.s));
+        *xw = wgt;
+        if constexpr (BwdExchange<FAM>::kPair) {
+            const float da = hit ? d_alpha : 0.f;
+            *reinterpret_cast<float2*>(xyz) = make_float2(da * w, da * s1.y * dwdm);
+        } else {
+            *xyz = d_alpha * w;
+        }
+        px.s = fmaf(gc, wgt, px.s);
+        if (hit) px.T = t_before;
+        return;
+    }
     float alpha = fminf(kAlphaClampF, a_raw);
     bool gate = a_raw < kAlphaClampF;
     if constexpr (CAREFUL) {
@@ -746,6 +795,10 @@ render_bwd_kernel(KParams kp, const float4* __restrict__ recs, const int2* __res
         }
         mbar_wait(bar + stage, parity);
         const float4* qc = stage0 + stage * kChunkVecs;
+        // entry `lane` of the chunk: can its alpha reach the clamp?  (bits of batches that do not run
+        // may cover bytes beyond the stream's padding; they are not looked at)
+        const unsigned clampable =
+            FAM == FAM_GENERIC ? kFull : __ballot_sync(kFull, !(qc[lane * kEntryVecs + 1].y < kClampableF));
         const int first = used - c * kChunk > kBwdBatch ? 1 : 0;  // upper batch holds composited entries?
         for (int h = first; h >= 0; --h) {
             const float4* qb = qc + h * (kBwdBatch * kEntryVecs);
@@ -753,15 +806,22 @@ render_bwd_kernel(KParams kp, const float4* __restrict__ recs, const int2* __res
             for (int j0 = kBwdBatch - kGroup; j0 >= 0; j0 -= kGroup) {
                 const BwdPixel save = px;
                 bool near_acc = false;
+                if ((clampable >> (h * kBwdBatch + j0)) & ((1u << kGroup) - 1u)) {
 #pragma unroll
-                for (int j = kGroup - 1; j >= 0; --j)
-                    bwd_visit<FAM, false>(kp, recs, qb + (j0 + j) * 3, fx, fy, px, ww + j0 + j,
-                                          wyz + kYzWords * (j0 + j), near_acc);
+                    for (int j = kGroup - 1; j >= 0; --j)
+                        bwd_visit<FAM, false, true>(kp, recs, qb + (j0 + j) * 3, fx, fy, px, ww + j0 + j,
+                                                    wyz + kYzWords * (j0 + j), near_acc);
+                } else {
+#pragma unroll
+                    for (int j = kGroup - 1; j >= 0; --j)
+                        bwd_visit<FAM, false, false>(kp, recs, qb + (j0 + j) * 3, fx, fy, px, ww + j0 + j,
+                                                     wyz + kYzWords * (j0 + j), near_acc);
+                }
                 if (kp.exact && __any_sync(kFull, near_acc)) {  // a few groups per thousand
                     px = save;
                     for (int j = kGroup - 1; j >= 0; --j)
-                        bwd_visit<FAM, true>(kp, recs, qb + (j0 + j) * 3, fx, fy, px, ww + j0 + j,
-                                             wyz + kYzWords * (j0 + j), near_acc);
+                        bwd_visit<FAM, true, true>(kp, recs, qb + (j0 + j) * 3, fx, fy, px, ww + j0 + j,
+                                                   wyz + kYzWords * (j0 + j), near_acc);
                 }
             }
             __syncwarp();

@@ -139,9 +139,20 @@ def oracle_kernel(port, name):
     return k
 
 
-def run_forward_parity(ctx, port, name, n, w, h, seed, bg=BG):
+def make_opaque(s, seed):
+    """Opacities in [0.9, 1]: about one splat in five can reach the 0.99 alpha clamp
+    (rasterizer.cpp:93, :202), so groups with and without such entries alternate in every stream."""
+    rng = np.random.default_rng(seed)
+    s.opacity[:] = f32(rng.uniform(0.9, 1.0, size=s.opacity.shape))
+    s.opacity[::17] = 1.0
+    return s
+
+
+def run_forward_parity(ctx, port, name, n, w, h, seed, bg=BG, opaque=False):
     k = oracle_kernel(port, name)
     s = port.random_scene(k, n, w, h, seed)
+    if opaque:
+        make_opaque(s, seed)
     ref = port.forward(k, s, w, h, bg, threads=0)
     out = ctx.forward(gpu_kernel_cached(name), **scene_f32(s), width=w, height=h, background=bg)
     assert np.array_equal(out["processed"], ref["processed"]), "processed differs"
@@ -176,6 +187,13 @@ def test_forward_parity_ragged_dense(ctx, port, name):
     """Image not a multiple of the tile size, lists longer than one 32-entry chunk, early
     termination on most pixels."""
     run_forward_parity(ctx, port, name, 3000, 77, 45, 11)
+
+
+@pytest.mark.parametrize("name", KERNELS + GENERIC[:1])
+def test_forward_parity_opaque(ctx, port, name):
+    """Splats that reach the alpha clamp mixed with splats that cannot (the render kernels run
+    a clamp-free variant on groups of entries whose opacity is below 0.98)."""
+    run_forward_parity(ctx, port, name, 2500, 90, 70, 13, opaque=True)
 
 
 def test_forward_config1_bit_exact_counts(ctx, port):
@@ -248,9 +266,11 @@ def grad_err(got, ref):
     return rel_err(got, ref, floor)
 
 
-def run_backward_parity(ctx, port, name, n, w, h, seed, gseed=32):
+def run_backward_parity(ctx, port, name, n, w, h, seed, gseed=32, opaque=False):
     k = oracle_kernel(port, name)
     s = port.random_scene(k, n, w, h, seed)
+    if opaque:
+        make_opaque(s, seed)
     g = port.random_image_grad(w, h, gseed)
     fr = port.forward(k, s, w, h, BG, threads=0, keep=True)
     st, ref = port.backward(fr["handle"], k, g, s, threads=0)
@@ -280,6 +300,13 @@ def test_backward_parity_small(ctx, port, name, seed):
 @pytest.mark.parametrize("name", KERNELS + GENERIC)
 def test_backward_parity_ragged_dense(ctx, port, name):
     run_backward_parity(ctx, port, name, 3000, 77, 45, 11)
+
+
+@pytest.mark.parametrize("name", KERNELS + GENERIC[:1])
+def test_backward_parity_opaque(ctx, port, name):
+    """The alpha clamp blocks the gradient through alpha (rasterizer.cpp:202): clamped and
+    unclamped entries mixed in every stream."""
+    run_backward_parity(ctx, port, name, 2500, 90, 70, 13, opaque=True)
 
 
 def test_backward_config1(ctx, port):
