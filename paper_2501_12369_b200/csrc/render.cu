@@ -12,7 +12,7 @@
 //                 quadratic form over the block against the splat's decision
 //                 threshold).  Survivors are written, in list order, to one compact
 //                 stream per block as ready-to-composite 48-byte entries
-//                 { mu.x, mu.y, A, B } { C, opacity, thr_m, list position }
+//                 { mu.x, mu.y, A, C } { B, opacity, thr_m, list position }
 //                 { r, g, b, splat index }.
 //   render_fwd    a warp streams its block's entries into shared memory with 1-D
 //                 bulk async copies (cp.async.bulk + mbarrier: UBLKCP in SASS), three
@@ -111,8 +111,12 @@ __device__ __forceinline__ void generic_eval(const KParams& kp, float dm2, float
 // { clamped alpha, weight, d weight / d m, flags } with flags bit 0 = the visit
 // contributes, bit 1 = alpha_raw < 0.99 (the clamp lets the gradient through,
 // rasterizer.cpp:202).  Out of line: taken for a few visits per million.
-__device__ __noinline__ float4 exact_decide(const KParams& kp, const float4* __restrict__ recs,
-                                            int idx, float fx, float fy) {
+struct ExactVisit {
+    double alpha, w, dw;  // clamped alpha, weight, d weight / d dm2
+    bool hit, unclamped;
+};
+__device__ __forceinline__ ExactVisit exact_visit(const KParams& kp, const float4* __restrict__ recs, int idx,
+                                                  float fx, float fy) {
     const float4 v0 = __ldg(recs + kRecVecs * (int64_t)idx);
     const float4 v1 = __ldg(recs + kRecVecs * (int64_t)idx + 1);
     const float4 v3 = __ldg(recs + kRecVecs * (int64_t)idx + 3);
@@ -121,18 +125,102 @@ __device__ __noinline__ float4 exact_decide(const KParams& kp, const float4* __r
     double dm2 = __dadd_rn(__dadd_rn(__dmul_rn(__dmul_rn(a, dx), dx),
                                      __dmul_rn(__dmul_rn(__dmul_rn(2.0, b), dx), dy)),
                            __dmul_rn(__dmul_rn(c, dy), dy));
+    ExactVisit v;
+    v.alpha = v.w = v.dw = 0.0;
+    v.hit = v.unclamped = false;
+    if (!(dm2 >= 0.0)) return v;  // dm2 < 0 (or NaN, which the reference rejects)
+    eval_exact(kp, dm2, v.w, v.dw);
+    const double alpha_raw = o * v.w;
+    const double alpha = fmin(kAlphaClampD, alpha_raw);
+    if (alpha < kAlphaSkipD) return v;
+    v.alpha = alpha;
+    v.hit = true;
+    v.unclamped = alpha_raw < kAlphaClampD;
+    return v;
+}
+
+__device__ __noinline__ float4 exact_decide(const KParams& kp, const float4* __restrict__ recs,
+                                            int idx, float fx, float fy) {
+    const ExactVisit v = exact_visit(kp, recs, idx, fx, fy);
     float4 out = make_float4(0.f, 0.f, 0.f, __int_as_float(0));
-    if (!(dm2 >= 0.0)) return out;  // dm2 < 0 (or NaN, which the reference rejects)
-    double w, dw;
-    eval_exact(kp, dm2, w, dw);
-    double alpha_raw = o * w;
-    double alpha = fmin(kAlphaClampD, alpha_raw);
-    if (alpha < kAlphaSkipD) return out;
-    out.x = (float)alpha;
-    out.y = (float)w;
-    out.z = (float)(dw / (double)kp.scale);
-    out.w = __int_as_float(1 | (alpha_raw < kAlphaClampD ? 2 : 0));
+    if (!v.hit) return out;
+    out.x = (float)v.alpha;
+    out.y = (float)v.w;
+    out.z = (float)(v.dw / (double)kp.scale);
+    out.w = __int_as_float(1 | (v.unclamped ? 2 : 0));
     return out;
+}
+
+// One pixel composited in FP64 as the reference does it (rasterizer.cpp:85-107), by the whole
+// warp: lane j evaluates entry base + j of the block's stream, a warp scan gives every entry the
+// transmittance in front of it, and the first entry that takes it below the floor ends the walk.
+// Called for the few pixels per thousand whose FP32 transmittance came within the guard band of
+// the floor, where the FP32 value cannot say which entry was the last (rasterizer.cpp:100).  The
+// factors (1 - alpha) are the reference's; only the association of their product differs (the
+// scan), a relative 1e-15 against a guard band of 1e-5.  Entries culled at block level cannot
+// contribute, so the stream holds every entry that matters.
+struct ExactPixel {
+    double T, c0, c1, c2;
+    int processed, contributors, stream_end;  // stream_end: entries of the stream the pixel consumed
+};
+__device__ __noinline__ ExactPixel exact_pixel(const KParams& kp, const float4* __restrict__ recs,
+                                               const float4* __restrict__ stream, int n, int list_len,
+                                               float fx, float fy, int lane) {
+    constexpr unsigned kAll = 0xffffffffu;
+    ExactPixel r;
+    r.T = 1.0;
+    r.contributors = 0;
+    r.processed = list_len;
+    r.stream_end = n;
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0;  // this lane's share of the colour
+    for (int base = 0; base < n; base += 32) {
+        const int e = base + lane;
+        ExactVisit v;
+        v.alpha = 0.0;
+        v.hit = false;
+        float4 s2 = make_float4(0.f, 0.f, 0.f, 0.f);
+        int pos = 0;
+        if (e < n) {
+            s2 = __ldg(stream + (size_t)e * 3 + 2);
+            pos = __float_as_int(__ldg(stream + (size_t)e * 3 + 1).w);
+            if (__float_as_int(s2.w) >= 0) v = exact_visit(kp, recs, __float_as_int(s2.w), fx, fy);
+        }
+        double P = 1.0 - v.alpha;  // inclusive prefix product of the factors (alpha = 0: no hit)
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const double t = __shfl_up_sync(kAll, P, d);
+            if (lane >= d) P *= t;
+        }
+        double before = __shfl_up_sync(kAll, P, 1);
+        before = r.T * (lane == 0 ? 1.0 : before);
+        const double after = r.T * P;
+        const unsigned hits = __ballot_sync(kAll, v.hit);
+        const unsigned cross = __ballot_sync(kAll, v.hit && after < 1e-4);  // kTransmittanceFloor
+        const int jc = cross ? __ffs(cross) - 1 : 31;
+        if (v.hit && lane <= jc) {
+            const double at = v.alpha * before;
+            a0 += (double)s2.x * at;
+            a1 += (double)s2.y * at;
+            a2 += (double)s2.z * at;
+        }
+        r.contributors += __popc(hits & (0xffffffffu >> (31 - jc)));
+        r.T = __shfl_sync(kAll, after, jc);
+        if (cross) {
+            r.processed = __shfl_sync(kAll, pos, jc) + 1;
+            r.stream_end = base + jc + 1;
+            break;
+        }
+    }
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) {
+        a0 += __shfl_xor_sync(kAll, a0, d);
+        a1 += __shfl_xor_sync(kAll, a1, d);
+        a2 += __shfl_xor_sync(kAll, a2, d);
+    }
+    r.c0 = a0;
+    r.c1 = a1;
+    r.c2 = a2;
+    return r;
 }
 
 // FP32 decision of one (pixel, entry) visit.  m = scaled squared Mahalanobis
@@ -169,8 +257,14 @@ __device__ __forceinline__ void fast_decide(const KParams& kp, float m, float th
     }
 }
 
-__device__ __forceinline__ float quad_m(float A, float B, float C, float dx, float dy) {
-    return fmaf(fmaf(A, dx, B * dy), dx, (C * dy) * dy);
+// m = A dx^2 + B dx dy + C dy^2 for a record / stream entry { mu.x, mu.y, A, C } { B, ... }: the
+// pairs (A, C) and (dx, dy) meet in one packed multiply, four instructions in all.  d = mu - centre
+// (the form is even).  Forward and backward share this exact sequence, so both passes see the
+// same bits and take identical decisions.
+__device__ __forceinline__ float quad_m(const float4& e0, float B, float2 neg_centre) {
+    const float2 d = __fadd2_rn(make_float2(e0.x, e0.y), neg_centre);
+    const float2 pq = __fmul2_rn(make_float2(e0.z, e0.w), d);  // (A dx, C dy)
+    return fmaf(fmaf(B, d.x, pq.y), d.y, pq.x * d.x);
 }
 
 
@@ -289,7 +383,7 @@ cull_kernel(KParams kp, const float4* __restrict__ recs, const int2* __restrict_
                 const float dyc = fminf(fmaxf(0.f, ey0), ey1);
 #pragma unroll
                 for (int xb = 0; xb < 2; ++xb)
-                    if (block_survives(v0.z, v0.w, v1.x, v1.w, v2.w, thr2, dxc[xb], ex0[xb], ex1[xb], dyc, ey0,
+                    if (block_survives(v0.z, v1.x, v0.w, v1.w, v2.w, thr2, dxc[xb], ex0[xb], ex1[xb], dyc, ey0,
                                        ey1))
                         bits |= 1u << (yb * 2 + xb);
             }
@@ -417,10 +511,30 @@ __device__ __forceinline__ void fwd_visit(const KParams& kp, const float4* __res
     const float4 s0 = qe[0];
     const float4 s1 = qe[1];
     const float4 s2 = qe[2];
-    // (mu - centre): the quadratic form is even, and the packed add takes no negated operand
-    const float2 d = __fadd2_rn(make_float2(s0.x, s0.y), make_float2(-fx, -fy));
-    const float dx = d.x, dy = d.y;
-    const float m = quad_m(s0.z, s0.w, s1.x, dx, dy);
+    const float m = quad_m(s0, s1.x, make_float2(-fx, -fy));
+    if constexpr (!CAREFUL && FAM != FAM_GENERIC) {
+        // The speculative form, two instructions shorter than what the compiler makes of the
+        // general one below: take = (thr > m) && live selects alpha, and both counters (visits met
+        // while live, contributors) are predicated adds.  live = !(T < floor), as below.
+        near_acc = near_acc || !(fabsf(s1.z - m) > kp.band);  // also true for a NaN threshold
+        const float a_raw = s1.y * fam_weight<FAM>(m);
+        float alpha = CLAMP ? fminf(kAlphaClampF, a_raw) : a_raw;
+        asm("{\n\t"
+            ".reg .pred p, q;\n\t"
+            "setp.geu.f32 p, %5, %6;\n\t"
+            "setp.gt.and.f32 q, %3, %4, p;\n\t"
+            "@p add.s32 %1, %1, 1;\n\t"
+            "@q add.f32 %2, %2, 0f3F800000;\n\t"
+            "selp.f32 %0, %0, 0f00000000, q;\n\t"
+            "}"
+            : "+f"(alpha), "+r"(px.nlive), "+f"(px.contrib)
+            : "f"(s1.z), "f"(m), "f"(px.T), "f"(kTFloorF));
+        const float at = alpha * px.T;
+        px.crg = __ffma2_rn(make_float2(s2.x, s2.y), make_float2(at, at), px.crg);
+        px.cb = fmaf(s2.z, at, px.cb);
+        px.T = fmaf(-alpha, px.T, px.T);
+        return;
+    }
     const bool live = !(px.T < kTFloorF);
     bool hit, near;
     float a_raw, w, dwdm;
@@ -436,13 +550,13 @@ __device__ __forceinline__ void fwd_visit(const KParams& kp, const float4* __res
     } else {
         near_acc = near_acc || near;
     }
-    const float hitf = (hit && live) ? 1.f : 0.f;
-    alpha *= hitf;
+    const bool take = hit && live;
+    alpha = take ? alpha : 0.f;
     // rasterizer.cpp:96-100
     const float at = alpha * px.T;
     px.crg = __ffma2_rn(make_float2(s2.x, s2.y), make_float2(at, at), px.crg);
     px.cb = fmaf(s2.z, at, px.cb);
-    px.contrib += hitf;
+    px.contrib += take ? 1.f : 0.f;
     // T never rises and a dead lane blends alpha = 0, so the entries a lane meets while live are a
     // prefix of the stream and the last of them is the one that crossed the floor
     if (live) ++px.nlive;
@@ -557,36 +671,58 @@ render_fwd_kernel(KParams kp, const float4* __restrict__ recs, const int2* __res
             ++stage;
         }
     }
-    // pixels whose transmittance came within the guard band of the floor: the last value
-    // (the first below the floor, or the final one) and, for a pixel that crossed, the value
-    // just before the crossing, recovered from the splat that crossed it
-    unsigned nfloor = 0;
+    // Pixels whose transmittance came within the guard band of the floor: the last value (the first
+    // below the floor, or the final one) and, for a pixel that crossed, the value just before the
+    // crossing, recovered from the entry that crossed it.  FP32 cannot say on which entry such a
+    // pixel stopped; it is composited again in FP64 by the whole warp (exact_pixel).
+    bool flagged = false;
+    int proc = end - beg;  // processed (rasterizer.cpp:86,100): the whole list, or up to the entry that crossed
+    float out_r = fmaf(bg0, px.T, px.crg.x), out_g = fmaf(bg1, px.T, px.crg.y), out_b = fmaf(bg2, px.T, px.cb);
+    float out_t = px.T;
+    int out_contrib = (int)px.contrib;
     if (inside) {
-        nfloor = fabsf(px.T - kTFloorF) < 2e-9f;
-        // processed (rasterizer.cpp:86,100): the whole list, or up to the entry that crossed the floor
-        int proc = end - beg;
+        flagged = fabsf(px.T - kTFloorF) < 2e-9f;
         if (px.T < kTFloorF && px.nlive > 0) {
             const float4 v0 = __ldg(src + (size_t)(px.nlive - 1) * kEntryVecs);
             const float4 v1 = __ldg(src + (size_t)(px.nlive - 1) * kEntryVecs + 1);
             proc = __float_as_int(v1.w) + 1;
             bool hit, near;
             float a_raw, w, dwdm;
-            fast_decide<FAM, false>(kp, quad_m(v0.z, v0.w, v1.x, fx - v0.x, fy - v0.y), v1.z, v1.y, hit, near,
+            fast_decide<FAM, false>(kp, quad_m(v0, v1.x, make_float2(-fx, -fy)), v1.z, v1.y, hit, near,
                                     a_raw, w, dwdm);
             const float t_cross = px.T / (1.0f - fminf(kAlphaClampF, a_raw));
-            nfloor = nfloor || fabsf(t_cross - kTFloorF) < 4e-9f;
+            flagged = flagged || fabsf(t_cross - kTFloorF) < 4e-9f;
         }
+    }
+    unsigned todo = kp.exact ? __ballot_sync(kFull, flagged) : 0u;
+    const unsigned nfloor = __popc(__ballot_sync(kFull, flagged));
+    while (todo) {
+        const int l = __ffs(todo) - 1;
+        todo &= todo - 1;
+        const ExactPixel ep = exact_pixel(kp, recs, src, n, end - beg, __shfl_sync(kFull, fx, l),
+                                          __shfl_sync(kFull, fy, l), lane);
+        // the backward walks [0, used): it must reach the entry this pixel stopped on
+        used = max(used, (ep.stream_end + kGroup - 1) & ~(kGroup - 1));
+        if (lane == l) {
+            out_r = (float)(ep.c0 + (double)bg0 * ep.T);
+            out_g = (float)(ep.c1 + (double)bg1 * ep.T);
+            out_b = (float)(ep.c2 + (double)bg2 * ep.T);
+            out_t = (float)ep.T;
+            proc = ep.processed;
+            out_contrib = ep.contributors;
+        }
+    }
+    if (inside) {
         size_t p = (size_t)pyl * W + pxl;
-        image[p * 3 + 0] = fmaf(bg0, px.T, px.crg.x);
-        image[p * 3 + 1] = fmaf(bg1, px.T, px.crg.y);
-        image[p * 3 + 2] = fmaf(bg2, px.T, px.cb);
-        t_final[p] = px.T;
+        image[p * 3 + 0] = out_r;
+        image[p * 3 + 1] = out_g;
+        image[p * 3 + 2] = out_b;
+        t_final[p] = out_t;
         processed[p] = proc;
-        contributors[p] = (int)px.contrib;
+        contributors[p] = out_contrib;
     }
     // instrumentation: one atomic per warp per counter
     const unsigned nexact = __reduce_add_sync(kFull, px.nexact);
-    nfloor = __reduce_add_sync(kFull, nfloor);
     if (lane == 0) {
         stream_used[tile * kBlocksPerTile + warp] = used;  // entries composited: all the backward needs
         atomicAdd(counters + CNT_COMPOSITED, (unsigned long long)used);
@@ -642,8 +778,7 @@ __device__ __forceinline__ void bwd_visit(const KParams& kp, const float4* __res
     const float4 s0 = qe[0];
     const float4 s1 = qe[1];
     const float4 s2 = qe[2];
-    const float dx = fx - s0.x, dy = fy - s0.y;
-    const float m = quad_m(s0.z, s0.w, s1.x, dx, dy);
+    const float m = quad_m(s0, s1.x, make_float2(-fx, -fy));
     const bool elig = __float_as_int(s1.w) < px.nproc;
     bool hit, near;
     float a_raw, w, dwdm;
@@ -886,8 +1021,8 @@ render_bwd_kernel(KParams kp, const float4* __restrict__ recs, const int2* __res
                     atomicAdd(reinterpret_cast<float4*>(dst), make_float4(dc0, dc1, dc2, dop));
                     atomicAdd(reinterpret_cast<float4*>(dst) + 1,
                               make_float4(kp.scale * sxx, 2.f * kp.scale * sxy, kp.scale * syy,
-                                          -fmaf(2.f * r0.z, sx, r0.w * sy)));
-                    atomicAdd(dst + 8, -fmaf(r0.w, sx, 2.f * r1.x * sy));
+                                          -fmaf(2.f * r0.z, sx, r1.x * sy)));
+                    atomicAdd(dst + 8, -fmaf(r1.x, sx, 2.f * r0.w * sy));
                 }
             }
             __syncwarp();

@@ -63,9 +63,10 @@ __device__ __forceinline__ void splat_record(const KParams& kp, float mx, float 
     // test and may produce dm2 < 0 (rasterizer.cpp:91): force the FP64 path.
     bool pd = (ad > 0.0) && (cd > 0.0) && (ad * cd - bd * bd > 0.0);
     float thr_m = pd ? (float)(thr * (double)kp.scale) : __int_as_float(0x7fc00000);
-    r[0] = make_float4(mx, my, kp.scale * a, kp.scale * (2.0f * b));
+    // (A, C) adjacent: they meet (dx, dy) in one packed multiply (quad_m, render.cu)
+    r[0] = make_float4(mx, my, kp.scale * a, kp.scale * c);
     // cull helpers: minimiser slope along the other axis, -B/(2C) and -B/(2A)
-    r[1] = make_float4(kp.scale * c, o, thr_m, -b / c);
+    r[1] = make_float4(kp.scale * (2.0f * b), o, thr_m, -b / c);
     r[2] = make_float4(cr, cg, cb, -b / a);
     r[3] = make_float4(a, b, c, 0.f);
 }
