@@ -22,9 +22,11 @@
 //   ssim_grad_kernel   the adjoint window over the zero-extended maps, then
 //                      grad = (1 - lambda) sign(d)/n + s_a + x s_e - d s_d, for pixels at least
 //                      five away from every edge.
-//   ssim_border_kernel pixels within five of an edge, where mirror padding folds taps back
+//   (border CTAs)      pixels within five of an edge, where mirror padding folds taps back
 //                      (loss.cpp:35-41, :76-103): the adjoint weights are enumerated exactly
-//                      with reflect().  Handles images smaller than the window too.
+//                      with reflect().  Handles images smaller than the window too.  They are
+//                      the first CTAs of the ssim_grad_kernel launch, so they run under the
+//                      interior tiles.
 //
 // Numerics (FP32 against the FP64 reference).  The reference's three partials d/d mu_x,
 // d/d s_xx, d/d s_xy (loss.cpp:133-138) and its combination s_a + 2 x s_b + y s_d (:222-224)
@@ -135,7 +137,7 @@ __device__ __forceinline__ void store12(float* __restrict__ p, int valid, const 
 
 // ---------------------------------------------------------------- moments + SSIM partials
 template <bool VEC>
-__global__ void __launch_bounds__(kLossThreads)
+__global__ void __launch_bounds__(kLossThreads, 5)
 ssim_map_kernel(Window win, int w, int h, const float* __restrict__ image,
                 const float* __restrict__ target, float scale, int want_maps,
                 float* __restrict__ fa, float* __restrict__ fe, float* __restrict__ fd,
@@ -286,16 +288,16 @@ ssim_map_kernel(Window win, int w, int h, const float* __restrict__ image,
 
 // ---------------------------------------------------------------- adjoint, interior pixels
 template <bool VEC>
-__global__ void __launch_bounds__(kLossThreads)
-ssim_grad_kernel(Window win, int w, int h, const float* __restrict__ image,
-                 const float* __restrict__ target, const float* __restrict__ fa,
-                 const float* __restrict__ fe, const float* __restrict__ fd, float coef_l1,
-                 float* __restrict__ grad) {
+__device__ __forceinline__ void grad_interior_tile(const Window& win, int w, int h, int tile_x, int tile_y,
+                                                   const float* __restrict__ image,
+                                                   const float* __restrict__ target, const float* __restrict__ fa,
+                                                   const float* __restrict__ fe, const float* __restrict__ fd,
+                                                   float coef_l1, float* __restrict__ grad) {
     __shared__ float2 s_v01[kTH * kCols];  // columns pass of (f_a, f_e)
     __shared__ float s_v2[kTH * kCols];    // columns pass of f_d
     __shared__ int s_row[kRowsIn];         // element offset of each input row, -1 outside the image
     const int tid = threadIdx.x;
-    const int x0 = blockIdx.x * kTW, y0 = blockIdx.y * kTH;
+    const int x0 = tile_x * kTW, y0 = tile_y * kTH;
     if (tid < kRowsIn) {
         const int gy = y0 - kHalf + tid;
         s_row[tid] = gy >= 0 && gy < h ? gy * w * 3 : -1;
@@ -416,14 +418,19 @@ __device__ __forceinline__ float adjoint_weight(const Window& win, int i, int j,
 
 constexpr int kBorderThreads = 128, kBorderLanes = 8;  // eight lanes share a pixel's 121 sources (measured faster than 32)
 
-__global__ void __launch_bounds__(kBorderThreads)
-ssim_border_kernel(Window win, int w, int h, int top, int bottom, int left, int right, int count,
-                   const float* __restrict__ image, const float* __restrict__ target,
-                   const float* __restrict__ fa, const float* __restrict__ fe,
-                   const float* __restrict__ fd, float coef_l1, float* __restrict__ grad) {
+struct BorderBand {
+    int top, bottom, left, right, count, blocks, stride;
+};
+
+__device__ __forceinline__ void grad_border_group(const Window& win, int w, int h, const BorderBand& band,
+                                                  int group, const float* __restrict__ image,
+                                                  const float* __restrict__ target, const float* __restrict__ fa,
+                                                  const float* __restrict__ fe, const float* __restrict__ fd,
+                                                  float coef_l1, float* __restrict__ grad) {
     __shared__ float s_w[kBorderThreads / kBorderLanes][2][kWin + 1];
+    const int top = band.top, bottom = band.bottom, left = band.left, right = band.right, count = band.count;
     const int slot = threadIdx.x / kBorderLanes, sub = threadIdx.x % kBorderLanes;
-    const int idx = blockIdx.x * (kBorderThreads / kBorderLanes) + slot;
+    const int idx = group * (kBorderThreads / kBorderLanes) + slot;
     const bool active = idx < count;
     int x = 0, y = 0;
     if (active) {
@@ -475,6 +482,26 @@ ssim_border_kernel(Window win, int w, int h, int top, int bottom, int left, int 
     }
 }
 
+// One launch for the whole adjoint: band.blocks CTAs, spread evenly over the grid, take the border
+// pixels (latency bound: 121 scattered sources per pixel), the others one interior tile each, so
+// the border work runs under the interior tiles instead of after them.
+static_assert(kBorderThreads == kLossThreads, "one CTA shape for both roles");
+template <bool VEC>
+__global__ void __launch_bounds__(kLossThreads)
+ssim_grad_kernel(Window win, int w, int h, BorderBand band, int tiles_x, const float* __restrict__ image,
+                 const float* __restrict__ target, const float* __restrict__ fa,
+                 const float* __restrict__ fe, const float* __restrict__ fd, float coef_l1,
+                 float* __restrict__ grad) {
+    // every band.stride-th CTA is a border one until they are used up
+    const int b = blockIdx.x, q = b / band.stride;
+    if (b - q * band.stride == 0 && q < band.blocks) {
+        grad_border_group(win, w, h, band, q, image, target, fa, fe, fd, coef_l1, grad);
+    } else {
+        const int t = b - min(q + 1, band.blocks);
+        grad_interior_tile<VEC>(win, w, h, t % tiles_x, t / tiles_x, image, target, fa, fe, fd, coef_l1, grad);
+    }
+}
+
 bool aligned16(const void* p) { return ((uintptr_t)p & 15u) == 0; }
 
 }  // namespace
@@ -514,26 +541,28 @@ darbs_status launch_loss(darbs_cuda_ctx* ctx, int width, int height, const float
         return launch_l1_loss(ctx, count, image, target, 0.0, grad_image, sums + 3);
     }
     const float coef = (float)((1.0 - lambda) / (double)count);  // loss.cpp:186
-    if (width > 2 * kHalf && height > 2 * kHalf) {
+    BorderBand band;
+    band.top = height < kHalf ? height : kHalf;
+    band.bottom = height - band.top < kHalf ? height - band.top : kHalf;
+    const int middle = height - band.top - band.bottom;
+    band.left = width < kHalf ? width : kHalf;
+    band.right = width - band.left < kHalf ? width - band.left : kHalf;
+    const long long border = (long long)(band.top + band.bottom) * width + (long long)middle * (band.left + band.right);
+    const int per_block = kBorderThreads / kBorderLanes;
+    band.count = (int)border;
+    band.blocks = (int)((border + per_block - 1) / per_block);
+    // interior tiles exist only when some pixel is five or more from every edge
+    const bool interior = width > 2 * kHalf && height > 2 * kHalf;
+    const unsigned blocks = (unsigned)band.blocks + (interior ? grid.x * grid.y : 0u);
+    band.stride = band.blocks ? (int)(blocks / (unsigned)band.blocks) : 1;
+    if (blocks) {
         if (vec)
-            ssim_grad_kernel<true><<<grid, kLossThreads, 0, ctx->stream>>>(win, width, height, image, target, fa,
-                                                                           fe, fd, coef, grad_image);
+            ssim_grad_kernel<true><<<blocks, kLossThreads, 0, ctx->stream>>>(win, width, height, band, (int)grid.x, image,
+                                                                             target, fa, fe, fd, coef, grad_image);
         else
-            ssim_grad_kernel<false><<<grid, kLossThreads, 0, ctx->stream>>>(win, width, height, image, target, fa,
-                                                                            fe, fd, coef, grad_image);
+            ssim_grad_kernel<false><<<blocks, kLossThreads, 0, ctx->stream>>>(win, width, height, band, (int)grid.x, image,
+                                                                              target, fa, fe, fd, coef, grad_image);
         DARBS_TRY(check_launch(ctx, "ssim_grad_kernel"));
-    }
-    const int top = height < kHalf ? height : kHalf;
-    const int bottom = height - top < kHalf ? height - top : kHalf;
-    const int middle = height - top - bottom;
-    const int left = width < kHalf ? width : kHalf;
-    const int right = width - left < kHalf ? width - left : kHalf;
-    const long long band = (long long)(top + bottom) * width + (long long)middle * (left + right);
-    if (band > 0) {
-        const int per_block = kBorderThreads / kBorderLanes;
-        ssim_border_kernel<<<(unsigned)((band + per_block - 1) / per_block), kBorderThreads, 0, ctx->stream>>>(
-            win, width, height, top, bottom, left, right, (int)band, image, target, fa, fe, fd, coef, grad_image);
-        DARBS_TRY(check_launch(ctx, "ssim_border_kernel"));
     }
     return DARBS_OK;
 }

@@ -810,7 +810,7 @@ __device__ __forceinline__ void bwd_visit(const KParams& kp, const float4* __res
             *xyz = d_alpha * w;
         }
         px.s = fmaf(gc, wgt, px.s);
-        if (hit) px.T = t_before;
+        px.T = t_before;  // a lane that does not take the entry: alpha = 0, rcp(1) = 1 exactly
         return;
     }
     float alpha = fminf(kAlphaClampF, a_raw);
@@ -846,7 +846,7 @@ __device__ __forceinline__ void bwd_visit(const KParams& kp, const float4* __res
     else
         *xyz = da * w;
     px.s = fmaf(gc, wgt, px.s);
-    if (hit) px.T = t_before;
+    px.T = t_before;  // a lane that does not take the entry: alpha = 0, rcp(1) = 1 exactly
 }
 
 template <int FAM>
