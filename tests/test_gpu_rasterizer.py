@@ -196,6 +196,18 @@ def test_forward_parity_opaque(ctx, port, name):
     run_forward_parity(ctx, port, name, 2500, 90, 70, 13, opaque=True)
 
 
+def test_transmittance_floor_pixels_are_exact(ctx, port):
+    """The last decision of a pixel, T < 1e-4 (rasterizer.cpp:100), cannot be taken in FP32 when T
+    ends within a few 1e-9 of the floor: the forward kernel composites those pixels again in FP64
+    (counted in work_counters().tfloor).  Dense scenes over several seeds so that the path runs."""
+    flagged = 0
+    for name in ("gaussian", "raised-cosine", "inv-multiquadratic"):
+        for seed in (11, 12, 13):
+            run_forward_parity(ctx, port, name, 3000, 77, 45, seed)
+            flagged += ctx.work_counters()["tfloor"]
+    assert flagged > 0
+
+
 def test_forward_config1_bit_exact_counts(ctx, port):
     """BASELINE config 1: 10k splats, 256x256, half-cosine-squared."""
     s, ref, out = run_forward_parity(ctx, port, "half-cosine-sq", 10000, 256, 256, 0)
