@@ -751,6 +751,9 @@ render_fwd_kernel(KParams kp, const float4* __restrict__ recs, const int2* __res
 constexpr int kBwdWarps = 1;
 constexpr int kBwdThreads = 32 * kBwdWarps;
 constexpr int kBwdBatch = 16;
+// Stages of the bulk-copy ring: one chunk (32 entries, a few thousand cycles of compositing) of
+// prefetch distance hides the copy; the third stage of the forward would cost resident CTAs here.
+constexpr int kBwdStages = 2;
 static_assert(kPad % kBwdBatch == 0 && kPad % kGroup == 0 && kChunk % kPad == 0, "stream padding covers every loop unit");
 constexpr int kXStride = kBwdBatch + 1;  // odd: conflict-free both by row and by column
 constexpr int kSplatGradStride = 12;     // internal gradient rows are padded to 12 floats for 128-bit atomics
@@ -850,14 +853,14 @@ __device__ __forceinline__ void bwd_visit(const KParams& kp, const float4* __res
 }
 
 template <int FAM>
-__global__ void __launch_bounds__(kBwdThreads, 16 / kBwdWarps)
+__global__ void __launch_bounds__(kBwdThreads, 24 / kBwdWarps)
 render_bwd_kernel(KParams kp, const float4* __restrict__ recs, const int2* __restrict__ ranges,
                   const float4* __restrict__ streams, const int* __restrict__ stream_used, int W, int H,
                   int tiles_x, float bg0, float bg1, float bg2, const float* __restrict__ grad_image,
                   const float* __restrict__ t_final, const int* __restrict__ processed,
                   float* __restrict__ grads, unsigned long long* __restrict__ counters) {
-    __shared__ __align__(128) float4 ring[kBwdWarps][kStages][kChunkVecs];
-    __shared__ unsigned long long bars[kBwdWarps][kStages];
+    __shared__ __align__(128) float4 ring[kBwdWarps][kBwdStages][kChunkVecs];
+    __shared__ unsigned long long bars[kBwdWarps][kBwdStages];
     // [0]: wgt, then (y, z) pairs, or y alone for the Gaussian
     __shared__ __align__(16) float xch[kBwdWarps][BwdExchange<FAM>::kPair ? 3 : 2][32 * kXStride];
     __shared__ float4 gpix[kBwdWarps][32];
@@ -914,19 +917,21 @@ render_bwd_kernel(KParams kp, const float4* __restrict__ recs, const int2* __res
     float4* stage0 = ring[warp][0];
     unsigned long long* bar = bars[warp];
     if (lane == 0) {
-        for (int s = 0; s < kStages; ++s) mbar_init(bar + s);
+        for (int s = 0; s < kBwdStages; ++s) mbar_init(bar + s);
         mbar_init_fence();
-        if (nchunks > 0) bulk_load(stage0, src + (size_t)(nchunks - 1) * kChunkVecs, kChunkBytes, bar);
-        if (nchunks > 1)
-            bulk_load(stage0 + kChunkVecs, src + (size_t)(nchunks - 2) * kChunkVecs, kChunkBytes, bar + 1);
+        // the first kBwdStages - 1 chunks (from the back) in flight before the loop
+        for (int s = 0; s < kBwdStages - 1; ++s)
+            if (nchunks > s)
+                bulk_load(stage0 + s * kChunkVecs, src + (size_t)(nchunks - 1 - s) * kChunkVecs, kChunkBytes, bar + s);
     }
     __syncwarp();
     int stage = 0;
     unsigned parity = 0;
     for (int c = nchunks - 1; c >= 0; --c) {
-        if (lane == 0 && c >= 2) {
-            const int fill = stage == 0 ? 2 : stage - 1;
-            bulk_load(stage0 + fill * kChunkVecs, src + (size_t)(c - 2) * kChunkVecs, kChunkBytes, bar + fill);
+        if (lane == 0 && c >= kBwdStages - 1) {
+            const int fill = stage == 0 ? kBwdStages - 1 : stage - 1;  // the stage chunk c + 1 vacated
+            bulk_load(stage0 + fill * kChunkVecs, src + (size_t)(c - (kBwdStages - 1)) * kChunkVecs, kChunkBytes,
+                      bar + fill);
         }
         mbar_wait(bar + stage, parity);
         const float4* qc = stage0 + stage * kChunkVecs;
@@ -1027,7 +1032,7 @@ render_bwd_kernel(KParams kp, const float4* __restrict__ recs, const int2* __res
             }
             __syncwarp();
         }
-        if (stage == kStages - 1) {
+        if (stage == kBwdStages - 1) {
             stage = 0;
             parity ^= 1u;
         } else {
