@@ -479,7 +479,15 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned pari
 }
 
 // ------------------------------------------------------------------ forward
-constexpr int kGroup = 16;  // entries composited speculatively between two guard-band checks (8: +2 % on the forward)
+// Entries composited speculatively between two guard-band checks, and the granularity at which a
+// warp whose pixels have saturated leaves.  Measured per family: the Gaussian, most of whose
+// blocks run their whole stream, prefers 16 (half the per-group bookkeeping: -1 %); the families
+// whose pixels saturate early prefer 8 (fewer dead visits before the exit: -1 to -2 %).
+constexpr int kGroupMax = 16;
+template <int FAM>
+struct FwdGroup {
+    static constexpr int value = FAM == FAM_GAUSS2 ? 16 : 8;
+};
 
 // A pixel is live while its transmittance is at or above the floor
 // (rasterizer.cpp:100 leaves the loop the first time T < 1e-4); lanes outside
@@ -576,6 +584,7 @@ render_fwd_kernel(KParams kp, const float4* __restrict__ recs, const int2* __res
                   int tiles_x, float bg0, float bg1, float bg2, float* __restrict__ image,
                   float* __restrict__ t_final, int* __restrict__ processed, int* __restrict__ contributors,
                   unsigned long long* __restrict__ counters) {
+    constexpr int kGroup = FwdGroup<FAM>::value;
     __shared__ __align__(128) float4 ring[kFwdWarps][kStages][kChunkVecs];
     __shared__ unsigned long long bars[kFwdWarps][kStages];
     // the warp index through a warp reduction: the compiler then knows it is warp-uniform and
@@ -760,7 +769,7 @@ constexpr int kBwdGroup = 8;  // sweep 1's speculative unit (16 spills at the ba
 // Stages of the bulk-copy ring: one chunk (32 entries, a few thousand cycles of compositing) of
 // prefetch distance hides the copy; the third stage of the forward would cost resident CTAs here.
 constexpr int kBwdStages = 2;
-static_assert(kPad % kBwdBatch == 0 && kPad % kGroup == 0 && kBwdBatch % kBwdGroup == 0 && kChunk % kPad == 0,
+static_assert(kPad % kBwdBatch == 0 && kPad % kGroupMax == 0 && kBwdBatch % kBwdGroup == 0 && kChunk % kPad == 0,
               "stream padding covers every loop unit");
 constexpr int kXStride = kBwdBatch + 1;  // odd: conflict-free both by row and by column
 constexpr int kSplatGradStride = 12;     // internal gradient rows are padded to 12 floats for 128-bit atomics
