@@ -281,7 +281,6 @@ constexpr int kChunk = 32;
 constexpr int kPad = 16;
 constexpr int kChunkVecs = kChunk * kEntryVecs;
 constexpr int kChunkBytes = kChunkVecs * (int)sizeof(float4);
-constexpr int kStages = 3;
 
 // Entry offset of block `blk`'s stream for tile `tile` whose point list is [beg, end):
 // every block owns a region as long as the tile's list rounded up to a chunk (the
@@ -484,6 +483,13 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned pari
 // blocks run their whole stream, prefers 16 (half the per-group bookkeeping: -1 %); the families
 // whose pixels saturate early prefer 8 (fewer dead visits before the exit: -1 to -2 %).
 constexpr int kGroupMax = 16;
+// Stages of the forward's bulk-copy ring.  A block that saturates early leaves with the copies in
+// flight still to land and their bytes read for nothing: one chunk of prefetch distance for those
+// families, two for the Gaussian.
+template <int FAM>
+struct FwdStages {
+    static constexpr int value = FAM == FAM_GAUSS2 ? 3 : 2;
+};
 template <int FAM>
 struct FwdGroup {
     static constexpr int value = FAM == FAM_GAUSS2 ? 16 : 8;
@@ -585,8 +591,9 @@ render_fwd_kernel(KParams kp, const float4* __restrict__ recs, const int2* __res
                   float* __restrict__ t_final, int* __restrict__ processed, int* __restrict__ contributors,
                   unsigned long long* __restrict__ counters) {
     constexpr int kGroup = FwdGroup<FAM>::value;
-    __shared__ __align__(128) float4 ring[kFwdWarps][kStages][kChunkVecs];
-    __shared__ unsigned long long bars[kFwdWarps][kStages];
+    constexpr int kDepth = FwdStages<FAM>::value;  // stages of the bulk-copy ring
+    __shared__ __align__(128) float4 ring[kFwdWarps][kDepth][kChunkVecs];
+    __shared__ unsigned long long bars[kFwdWarps][kDepth];
     // the warp index through a warp reduction: the compiler then knows it is warp-uniform and
     // keeps the ring pointers and loop control in uniform registers
     const int lwarp = __reduce_min_sync(kFull, (int)(threadIdx.x >> 5)), lane = threadIdx.x & 31;
@@ -615,20 +622,20 @@ render_fwd_kernel(KParams kp, const float4* __restrict__ recs, const int2* __res
     float4* stage0 = ring[lwarp][0];
     unsigned long long* bar = bars[lwarp];
     if (lane == 0) {
-        for (int s = 0; s < kStages; ++s) mbar_init(bar + s);
+        for (int s = 0; s < kDepth; ++s) mbar_init(bar + s);
         mbar_init_fence();
-        // chunks 0 and 1 in flight before the loop; chunk c + 2 is issued while c is composited
-        if (nchunks > 0) bulk_load(stage0, src, kChunkBytes, bar);
-        if (nchunks > 1) bulk_load(stage0 + kChunkVecs, src + kChunkVecs, kChunkBytes, bar + 1);
+        // chunks 0 .. kDepth - 2 in flight before the loop; chunk c + kDepth - 1 is issued while c is composited
+        for (int s = 0; s < kDepth - 1; ++s)
+            if (nchunks > s) bulk_load(stage0 + s * kChunkVecs, src + (size_t)s * kChunkVecs, kChunkBytes, bar + s);
     }
     __syncwarp();
     int used = 0, stage = 0;
     unsigned parity = 0;
     int c = 0;
     for (; c < nchunks; ++c) {
-        if (lane == 0 && c + 2 < nchunks) {
-            const int fill = stage == 0 ? 2 : stage - 1;  // the stage chunk c - 1 vacated
-            bulk_load(stage0 + fill * kChunkVecs, src + (size_t)(c + 2) * kChunkVecs, kChunkBytes, bar + fill);
+        if (lane == 0 && c + kDepth - 1 < nchunks) {
+            const int fill = stage == 0 ? kDepth - 1 : stage - 1;  // the stage chunk c - 1 vacated
+            bulk_load(stage0 + fill * kChunkVecs, src + (size_t)(c + kDepth - 1) * kChunkVecs, kChunkBytes, bar + fill);
         }
         mbar_wait(bar + stage, parity);
         const float4* qc = stage0 + stage * kChunkVecs;
@@ -664,7 +671,7 @@ render_fwd_kernel(KParams kp, const float4* __restrict__ recs, const int2* __res
         }
         used += g * kGroup;
         __syncwarp();
-        if (stage == kStages - 1) {
+        if (stage == kDepth - 1) {
             stage = 0;
             parity ^= 1u;
         } else {
@@ -676,9 +683,9 @@ render_fwd_kernel(KParams kp, const float4* __restrict__ recs, const int2* __res
         }
     }
     // copies still in flight must land before the CTA's shared memory can be given away
-    for (int d = c; d < nchunks && d < c + 2; ++d) {
+    for (int d = c; d < nchunks && d < c + kDepth - 1; ++d) {
         mbar_wait(bar + stage, parity);
-        if (stage == kStages - 1) {
+        if (stage == kDepth - 1) {
             stage = 0;
             parity ^= 1u;
         } else {
