@@ -449,7 +449,10 @@ __global__ void adam_kernel(int64_t dim4, int64_t dim, float* __restrict__ param
                             const float* __restrict__ grads, float* __restrict__ m,
                             float* __restrict__ v, const float* __restrict__ lrs, float inv_bc1,
                             float inv_bc2) {
-    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    // Blocks walk the arrays from the end: the gradients param_grads_kernel wrote last are still in
+    // L2, and the parameters this kernel writes last (the front of the array) are the ones the next
+    // iteration's project_kernel reads first.
+    const int64_t i = (gridDim.x - 1 - blockIdx.x) * (int64_t)blockDim.x + threadIdx.x;
     if (i < dim4) {
         float4 p = reinterpret_cast<float4*>(params)[i];
         const float4 g = __ldg(reinterpret_cast<const float4*>(grads) + i);
