@@ -2,7 +2,7 @@
 //
 // TEST INFRASTRUCTURE, NOT PRODUCT.  oracle/Makefile compiles this file together
 // with the reference's own, unmodified sources
-//   /root/reference/proj/core/src/{kernel,geometry,rasterizer,loss}.cpp
+//   /root/reference/proj/core/src/{kernel,geometry,rasterizer,loss,fit3d,fit2d,scene_io,image}.cpp
 // (read where they lie; never copied) against oracle/eigen_shim into
 // oracle/_ref/libdarbs_ref.so.  It only marshals flat FP64 arrays into the
 // reference's types and back; no algorithm of the hot path is restated here
@@ -16,6 +16,8 @@
 #include <vector>
 
 #include "darbs/errors.hpp"
+#include "darbs/fit2d.hpp"
+#include "darbs/fit3d.hpp"
 #include "darbs/fit_common.hpp"
 #include "darbs/geometry.hpp"
 #include "darbs/kernel.hpp"
@@ -528,6 +530,139 @@ int darbs_cpu_adam_step(int64_t dim, double* params, const double* grads, double
     std::memcpy(m, st.m.data(), sizeof(double) * dim);
     std::memcpy(v, st.v.data(), sizeof(double) * dim);
     return DARBS_CPU_OK;
+}
+
+// ---- the callers of the hot path (reference build only): src/fit3d.cpp, src/fit2d.cpp.  Used by
+// tests/golden/make_golden.py to record the reference's own optimisation trajectories on
+// proj/data/demo_scene.txt + demo_cameras.txt, which the C++ mirror's fit_scene / fit_image
+// (paper_2501_12369_b200/host/darbs_b200_fit.hpp) are compared with on the GPU.
+namespace {
+
+void prim_to_flat(const Primitive3D& p, double* o) {
+    for (int k = 0; k < 3; ++k) o[k] = p.mu[k];
+    for (int k = 0; k < 3; ++k) o[3 + k] = p.scale[k];
+    o[6] = p.rot.w();
+    o[7] = p.rot.x();
+    o[8] = p.rot.y();
+    o[9] = p.rot.z();
+    o[10] = p.opacity;
+    for (int k = 0; k < 3; ++k) o[11 + k] = p.color[k];
+}
+
+FitConfig to_config(const double* cfg) {
+    // cfg = lambda, lr_position, lr_scale, lr_rotation, lr_opacity, lr_color, iters, seed, threads
+    FitConfig c;
+    c.lambda = cfg[0];
+    c.lr_position = cfg[1];
+    c.lr_scale = cfg[2];
+    c.lr_rotation = cfg[3];
+    c.lr_opacity = cfg[4];
+    c.lr_color = cfg[5];
+    c.iters = int(cfg[6]);
+    c.seed = std::uint64_t(cfg[7]);
+    c.threads = int(cfg[8]);
+    return c;
+}
+
+void report_out(const FitReport& r, double* curves, double* finals) {
+    // curves = [4][iters]: loss, l1, dssim, psnr; finals = mse, psnr, ssim
+    const std::size_t n = r.loss_curve.size();
+    for (std::size_t i = 0; i < n; ++i) {
+        curves[i] = r.loss_curve[i];
+        curves[n + i] = r.l1_curve[i];
+        curves[2 * n + i] = r.dssim_curve[i];
+        curves[3 * n + i] = r.psnr_curve[i];
+    }
+    finals[0] = r.final_mse;
+    finals[1] = r.final_psnr;
+    finals[2] = r.final_ssim;
+}
+
+}  // namespace
+
+// render_scene fit3d.cpp:29-40.  prims are realized (to_prim layout); image = 3*w*h.
+int darbs_cpu_render_scene(const darbs_cpu_kernel* k, double psi, int n, const double* prims,
+                           const double* camera, const double* background, int threads, double* image) {
+    try {
+        std::vector<Primitive3D> v;
+        for (int i = 0; i < n; ++i) v.push_back(to_prim(prims + 14 * std::size_t(i)));
+        ImageBuffer img = render_scene(v, to_camera(camera), to_spec(k), psi,
+                                       Vec3(background[0], background[1], background[2]), threads);
+        std::memcpy(image, img.rgb.data(), sizeof(double) * img.rgb.size());
+    } catch (...) {
+        return status_of_current_exception();
+    }
+    return DARBS_CPU_OK;
+}
+
+// fit_scene fit3d.cpp:42-203.  targets = n_views images of the cameras' sizes, concatenated.
+// curves must hold 4 * max(iters, 1) doubles, per_view_psnr n_views, out_prims 14 * n.
+int darbs_cpu_fit_scene(const darbs_cpu_kernel* k, double psi, int n, const double* init_prims, int n_views,
+                        const double* cameras22, const double* targets, const double* cfg, double* curves,
+                        double* finals, double* per_view_psnr, double* out_prims) {
+    try {
+        std::vector<Primitive3D> init;
+        for (int i = 0; i < n; ++i) init.push_back(to_prim(init_prims + 14 * std::size_t(i)));
+        std::vector<View> views;
+        const double* t = targets;
+        for (int v = 0; v < n_views; ++v) {
+            Camera cam = to_camera(cameras22 + 22 * std::size_t(v));
+            views.push_back(View{cam, to_image(cam.width, cam.height, t)});
+            t += std::size_t(3) * cam.width * cam.height;
+        }
+        Fit3DResult r = fit_scene(views, to_spec(k), psi, init, to_config(cfg));
+        report_out(r.report, curves, finals);
+        for (int v = 0; v < n_views; ++v) per_view_psnr[v] = r.per_view_psnr[v];
+        for (int i = 0; i < n; ++i) prim_to_flat(r.primitives[i], out_prims + 14 * std::size_t(i));
+    } catch (...) {
+        return status_of_current_exception();
+    }
+    return DARBS_CPU_OK;
+}
+
+// fit_image fit2d.cpp:45-188.  out_splats = 9 per splat (mu2, log_scale2, angle, opacity logit, colour logits 3).
+int darbs_cpu_fit_image(const darbs_cpu_kernel* k, int width, int height, const double* target, int n_splats,
+                        const double* cfg, double* curves, double* finals, double* rendered, double* out_splats) {
+    try {
+        Fit2DResult r = fit_image(to_image(width, height, target), to_spec(k), n_splats, to_config(cfg));
+        report_out(r.report, curves, finals);
+        std::memcpy(rendered, r.rendered.rgb.data(), sizeof(double) * r.rendered.rgb.size());
+        for (int i = 0; i < n_splats; ++i) {
+            const Splat2DParams& p = r.splats[i];
+            double* o = out_splats + 9 * std::size_t(i);
+            o[0] = p.mu2.x();
+            o[1] = p.mu2.y();
+            o[2] = p.log_scale.x();
+            o[3] = p.log_scale.y();
+            o[4] = p.angle;
+            o[5] = p.opacity_logit;
+            for (int c = 0; c < 3; ++c) o[6 + c] = p.color_logit[c];
+        }
+    } catch (...) {
+        return status_of_current_exception();
+    }
+    return DARBS_CPU_OK;
+}
+
+// read_cameras scene_io.cpp; returns the count (or a negative status).
+int darbs_cpu_read_cameras(const char* path, int capacity, double* cams22) {
+    try {
+        std::vector<Camera> v = read_cameras(path);
+        for (std::size_t i = 0; i < v.size() && int(i) < capacity; ++i) {
+            double* o = cams22 + 22 * i;
+            o[0] = v[i].fx;
+            o[1] = v[i].fy;
+            o[2] = v[i].cx;
+            o[3] = v[i].cy;
+            o[4] = v[i].width;
+            o[5] = v[i].height;
+            for (int r = 0; r < 4; ++r)
+                for (int c = 0; c < 4; ++c) o[6 + 4 * r + c] = v[i].w(r, c);
+        }
+        return int(v.size());
+    } catch (...) {
+        return -status_of_current_exception();
+    }
 }
 
 }  // extern "C"

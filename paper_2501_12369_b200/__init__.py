@@ -6,32 +6,24 @@ The product is the CUDA library ``libdarbs_cuda.so`` (sources in ``csrc/``, C AB
 tests and ``bench.py`` drive that ABI through; PyTorch is used for device
 memory, streams and ``torch.distributed`` — plumbing, not the product.
 
-There is NO CPU fallback: importing :mod:`paper_2501_12369_b200.api` raises if the
-CUDA library has not been built, and creating a context raises if no B200 is
+There is NO CPU fallback: :mod:`paper_2501_12369_b200.api` (loaded on first use of any name
+below) raises if the CUDA library has not been built, and creating a context raises if no B200 is
 visible.
 """
-from .api import (  # noqa: F401
-    DEVICE,
-    HOST,
-    Context,
-    DarbsError,
-    KernelSpec,
-    default_psi,
-    kernel_preset,
-    lib_path,
-    make_kernel,
-    version,
-)
+_API = ("DEVICE", "HOST", "Context", "DarbsError", "KernelSpec", "default_psi", "kernel_preset", "lib_path",
+        "make_kernel", "version")
 
-__all__ = [
-    "Context",
-    "DarbsError",
-    "KernelSpec",
-    "HOST",
-    "DEVICE",
-    "kernel_preset",
-    "make_kernel",
-    "default_psi",
-    "lib_path",
-    "version",
-]
+__all__ = list(_API)
+
+
+def __getattr__(name):
+    """The binding (and with it libdarbs_cuda.so) is loaded on first use of any of its names, so
+    that :mod:`paper_2501_12369_b200.synthetic` — pure numpy, the workload generator shared with
+    ``bench.py --impl reference`` — can be imported in a process that must not load the product
+    library.  Using the product without the built library still raises here."""
+    if name in _API or name == "api":
+        import importlib
+
+        api = importlib.import_module(".api", __name__)
+        return api if name == "api" else getattr(api, name)
+    raise AttributeError(f"module {__name__!r} has no attribute {name!r}")
