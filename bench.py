@@ -12,7 +12,7 @@ harmonic mean over the four kernels; per-kernel numbers are in ``per_kernel``.
 
   python bench.py [--gpus N] [--steps K] [--warmup W]            (torchrun for N > 1)
   python bench.py --impl reference ...   times the reference's own CPU code (oracle/_ref) on the
-                                         host cores on a bounded 1/16 sample of the same workload.
+                                         host cores on the same workload at full size (repetitions capped).
 """
 from __future__ import annotations
 
@@ -138,18 +138,25 @@ def cpu_iteration(orc, cpu, name, raw64, cam, target, lrs64, state, threads):
     return time.perf_counter() - t0, int(fr["processed"].sum())
 
 
-def cpu_setup(args):
+def cpu_setup(args, fraction):
+    """The CPU checker and the workload (fraction = 1: the GPU arm's own scene, camera and start;
+    otherwise a 1/fraction sample at equal splat density).  paper_2501_12369_b200.synthetic is pure
+    numpy: importing it does not load the product library (the package loads it lazily)."""
     from oracle import cpu
     from paper_2501_12369_b200 import synthetic as syn
 
     kind = "reference" if cpu.available("reference") else "port"
     orc = cpu.load(kind)
-    smp = syn.sample_workload(args.splats, args.width, args.height, args.focal, SAMPLE_FRACTION)
-    truth = syn.scene_b(smp["n"], 1, half_extent=smp["half_extent"])
-    cam = syn.orbit_camera(0, 1, smp["width"], smp["height"], smp["focal"])
+    if fraction == 1:
+        truth = syn.scene_b(args.splats, 1)
+        cam = syn.orbit_camera(0, 1, args.width, args.height, args.focal)
+    else:
+        smp = syn.sample_workload(args.splats, args.width, args.height, args.focal, fraction)
+        truth = syn.scene_b(smp["n"], 1, half_extent=smp["half_extent"])
+        cam = syn.orbit_camera(0, 1, smp["width"], smp["height"], smp["focal"])
     init = syn.perturb(truth, 2)
     lrs = syn.learning_rates(init)
-    return cpu, orc, kind, smp, truth, cam, init, lrs
+    return cpu, orc, kind, truth, cam, init, lrs
 
 
 def cpu_target(orc, cpu, name, truth, cam, threads):
@@ -164,37 +171,52 @@ def cpu_target(orc, cpu, name, truth, cam, threads):
 
 
 def run_reference_arm(args):
-    """--impl reference: the reference's own CPU implementation, all host threads."""
+    """--impl reference: the reference's own CPU implementation (oracle/_ref: its unmodified
+    kernel/geometry/rasterizer/loss sources), all host threads, on configs[2] AT FULL SIZE.  One
+    full-size iteration is 5-10 s of CPU time, so the arm caps its own repetitions (at most one
+    warm-up and two timed iterations per DARBF kernel; DARBS_REF_STEPS / DARBS_REF_WARMUP override)
+    and reports the steps it really ran, so that the whole run ends within a few minutes.  The 1/16
+    sample the GPU arm's ``cpu_baseline`` leg times is reported beside it as a secondary key."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
     threads = os.cpu_count() or 1
-    cpu, orc, kind, smp, truth, cam, init, lrs = cpu_setup(args)
+    steps = max(1, min(args.steps, int(os.environ.get("DARBS_REF_STEPS", "2"))))
+    warmup = max(0, min(args.warmup, int(os.environ.get("DARBS_REF_WARMUP", "1"))))
+    cpu, orc, kind, truth, cam, init, lrs = cpu_setup(args, fraction=1)
+    lrs64 = lrs.astype(np.float64)
     total, per_kernel = 0.0, {}
     for name in KERNELS:
         target = cpu_target(orc, cpu, name, truth, cam, threads)
         raw = init.astype(np.float64).copy()
         state = {"m": np.zeros(raw.size), "v": np.zeros(raw.size), "t": 0}
-        for _ in range(args.warmup):
-            cpu_iteration(orc, cpu, name, raw, cam, target, lrs.astype(np.float64), state, threads)
+        for _ in range(warmup):
+            cpu_iteration(orc, cpu, name, raw, cam, target, lrs64, state, threads)
         sec = 0.0
-        for _ in range(args.steps):
-            dt, _v = cpu_iteration(orc, cpu, name, raw, cam, target, lrs.astype(np.float64), state, threads)
+        for _ in range(steps):
+            dt, _v = cpu_iteration(orc, cpu, name, raw, cam, target, lrs64, state, threads)
             sec += dt
-        per_kernel[name] = {"ms_per_iter_sample": 1e3 * sec / args.steps,
-                            "iters_per_s_full_equiv": args.steps / sec / SAMPLE_FRACTION}
+        per_kernel[name] = {"ms_per_iter": 1e3 * sec / steps, "iters_per_s": steps / sec}
         total += sec
-    value = len(KERNELS) * args.steps / total / SAMPLE_FRACTION
-    sample = (f"1/{SAMPLE_FRACTION} of the workload at equal splat density: {smp['n']} primitives, "
-              f"{smp['width']}x{smp['height']}, full training iteration per kernel; value scaled by 1/{SAMPLE_FRACTION}")
+        del target, raw, state
+    value = len(KERNELS) * steps / total
+    sample = (f"the full workload ({args.splats} primitives, {args.width}x{args.height}), {warmup} warm-up + {steps} "
+              f"timed full training iterations per kernel ({args.steps} steps / {args.warmup} warm-up requested; "
+              f"capped so that the run ends within minutes)")
+    # secondary: the bounded 1/16 sample at equal splat density (what the GPU arm's cpu_baseline leg runs)
+    secondary = None
+    if not args.no_cpu_baseline:
+        cb = cpu_baseline(args, single_thread=False)
+        secondary = {"value_full_equiv": cb["value"], "sample": cb["sample"]}
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps * SAMPLE_FRACTION,
+        "steps": steps, "warmup": warmup, "steps_requested": args.steps, "warmup_requested": args.warmup,
+        "ms_per_step": 1e3 * total / steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": workload_config(args, args.gpus),
+        "config": workload_config(args, 1),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": kind, "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-        "per_kernel": per_kernel,
+        "per_kernel": per_kernel, "sample_1_16": secondary,
     }
     print(json.dumps(line), flush=True)
 
@@ -367,7 +389,7 @@ def run_ours(args):
         flops_fwd = V * (13 + fk) + 9 * Cn
         flops_bwd = V * (13 + fk + fpk) + 57 * Cn
         mufu_fwd, mufu_bwd = V * sk, V * (sk + spk) + Cn
-        fp32_peak = 2.0 * peaks["ffma_per_s"]
+        fp32_peak = fp32_peak_of(peaks)
 
         # the stricter count: only the lane-visits the kernels evaluate (32 lanes x composited entries)
         E = 32 * wc["composited"]
@@ -405,11 +427,13 @@ def run_ours(args):
     dk = per_kernel[dom[0]][dom[1]]
     roofline = {
         "bound": "fp32", "kernel": f"{dom[1]}<{dom[0]}>", "achieved": dk["achieved_tflops"],
-        "peak": 2.0 * peaks["ffma_per_s"] / 1e12, "unit": "TFLOP/s", "frac": dk["frac"],
+        "peak": fp32_peak_of(peaks) / 1e12, "unit": "TFLOP/s", "frac": dk["frac"],
         "traffic": ncu_traffic(f"{dom[1]}<{dom[0]}>"),
         "frac_fp32": dk["frac_fp32"], "frac_mufu": dk["frac_mufu"], "frac_evaluated": dk["frac_evaluated"],
-        "peak_source": "measured live by darbs_cuda_microbench (register-operand FFMA x2; MUFU ex2.approx); "
+        "peak_source": "measured live by darbs_cuda_microbench: the highest of register-operand FFMA, "
+                       "immediate-operand FFMA (x2 flops) and packed FFMA2 (x4 flops); MUFU ex2.approx; "
                        "MEASURED_PEAKS.json has no FP32/MUFU entry",
+        "peak_ffma_tflops": 2.0 * peaks["ffma_per_s"] / 1e12,
         "peak_mufu_gops": peaks["mufu_per_s"] / 1e9, "peak_sm_mhz": peaks["sm_mhz"],
         "peak_ffma_imm_tflops": 2.0 * peaks["ffma_imm_per_s"] / 1e12,
         "peak_ffma2_tflops": 4.0 * peaks["ffma2_per_s"] / 1e12,
@@ -472,6 +496,12 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
+def fp32_peak_of(peaks):
+    """FLOP/s of the FP32 pipe: the best of the three instruction forms the micro-benchmark times
+    (the render kernels issue FFMA2 where they can, so the packed rate is the honest denominator)."""
+    return max(2.0 * peaks["ffma_per_s"], 2.0 * peaks["ffma_imm_per_s"], 4.0 * peaks["ffma2_per_s"])
+
+
 def ncu_traffic(kernel):
     """DRAM bytes per launch of `kernel` from the committed ncu --set full capture (profiles/), or None."""
     try:
@@ -481,11 +511,13 @@ def ncu_traffic(kernel):
         return None
 
 
-def cpu_baseline(args):
-    """The reference's CPU code on this box's host cores, bounded to ~10-30 s: one training
-    iteration per kernel on the 1/16 sample (plus one warm-up for the first kernel)."""
+def cpu_baseline(args, single_thread=True):
+    """The reference's CPU code on this box's host cores, bounded to ~10-30 s: one or two training
+    iterations per kernel on a 1/16 sample at equal splat density, scaled by 1/16 (the full-size
+    figure is `bench.py --impl reference`)."""
     threads = os.cpu_count() or 1
-    cpu, orc, kind, smp, truth, cam, init, lrs = cpu_setup(args)
+    cpu, orc, kind, truth, cam, init, lrs = cpu_setup(args, fraction=SAMPLE_FRACTION)
+    lrs64 = lrs.astype(np.float64)
     total, iters = 0.0, 0
     t_budget = time.perf_counter()
     for name in KERNELS:
@@ -494,25 +526,27 @@ def cpu_baseline(args):
         state = {"m": np.zeros(raw.size), "v": np.zeros(raw.size), "t": 0}
         reps = 2 if time.perf_counter() - t_budget < 20 else 1
         for _ in range(reps):
-            dt, _v = cpu_iteration(orc, cpu, name, raw, cam, target, lrs.astype(np.float64), state, threads)
+            dt, _v = cpu_iteration(orc, cpu, name, raw, cam, target, lrs64, state, threads)
             total += dt
             iters += 1
     value = iters / total / SAMPLE_FRACTION
-    # the same sample on ONE host thread (SURVEY 8d asks for both): one iteration of the cheapest kernel
-    name = "half-cosine-sq"
-    target = cpu_target(orc, cpu, name, truth, cam, threads)
-    raw = init.astype(np.float64).copy()
-    state = {"m": np.zeros(raw.size), "v": np.zeros(raw.size), "t": 0}
-    dt1, _v = cpu_iteration(orc, cpu, name, raw, cam, target, lrs.astype(np.float64), state, 1)
-    raw = init.astype(np.float64).copy()
-    state = {"m": np.zeros(raw.size), "v": np.zeros(raw.size), "t": 0}
-    dtn, _v = cpu_iteration(orc, cpu, name, raw, cam, target, lrs.astype(np.float64), state, threads)
-    return {"value": value, "unit": UNIT, "cores": threads, "kind": kind,
-            "single_thread": {"kernel": name, "iters_per_s_full_equiv": 1.0 / dt1 / SAMPLE_FRACTION,
-                              "all_threads_iters_per_s_full_equiv": 1.0 / dtn / SAMPLE_FRACTION},
-            "sample": f"1/{SAMPLE_FRACTION} of the workload at equal splat density ({smp['n']} primitives, "
-                      f"{smp['width']}x{smp['height']}), {iters} full training iterations over the 4 kernels, "
-                      f"value scaled by 1/{SAMPLE_FRACTION}"}
+    out = {"value": value, "unit": UNIT, "cores": threads, "kind": kind,
+           "sample": f"1/{SAMPLE_FRACTION} of the workload at equal splat density ({truth.shape[0]} primitives, "
+                     f"{int(cam[4])}x{int(cam[5])}), {iters} full training iterations over the 4 kernels, "
+                     f"value scaled by 1/{SAMPLE_FRACTION}"}
+    if single_thread:
+        # the same sample on ONE host thread (SURVEY 8d asks for both): one iteration of the cheapest kernel
+        name = "half-cosine-sq"
+        target = cpu_target(orc, cpu, name, truth, cam, threads)
+        raw = init.astype(np.float64).copy()
+        state = {"m": np.zeros(raw.size), "v": np.zeros(raw.size), "t": 0}
+        dt1, _v = cpu_iteration(orc, cpu, name, raw, cam, target, lrs64, state, 1)
+        raw = init.astype(np.float64).copy()
+        state = {"m": np.zeros(raw.size), "v": np.zeros(raw.size), "t": 0}
+        dtn, _v = cpu_iteration(orc, cpu, name, raw, cam, target, lrs64, state, threads)
+        out["single_thread"] = {"kernel": name, "iters_per_s_full_equiv": 1.0 / dt1 / SAMPLE_FRACTION,
+                                "all_threads_iters_per_s_full_equiv": 1.0 / dtn / SAMPLE_FRACTION}
+    return out
 
 
 def main():

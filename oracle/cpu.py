@@ -121,6 +121,13 @@ class Oracle:
             lib.darbs_cpu_read_scene.argtypes = [C.c_char_p, C.c_int, _dp]
             lib.darbs_cpu_write_cameras.argtypes = [C.c_char_p, C.c_int, _dp]
             lib.darbs_cpu_write_image.argtypes = [C.c_char_p, C.c_int, C.c_int, _dp, C.c_int]
+        if hasattr(lib, "darbs_cpu_fit_scene"):  # the callers of the hot path: reference build only
+            lib.darbs_cpu_render_scene.argtypes = [C.POINTER(Kernel), C.c_double, C.c_int, _dp, _dp, _dp, C.c_int, _dp]
+            lib.darbs_cpu_fit_scene.argtypes = [C.POINTER(Kernel), C.c_double, C.c_int, _dp, C.c_int, _dp, _dp, _dp,
+                                                _dp, _dp, _dp, _dp]
+            lib.darbs_cpu_fit_image.argtypes = [C.POINTER(Kernel), C.c_int, C.c_int, _dp, C.c_int, _dp, _dp, _dp,
+                                                _dp, _dp]
+            lib.darbs_cpu_read_cameras.argtypes = [C.c_char_p, C.c_int, _dp]
 
     # ------------------------------------------------------------------ kernel
     @property
@@ -320,6 +327,52 @@ class Oracle:
     def write_image(self, path, img, ppm=False):
         img = _f64(img)
         return self.lib.darbs_cpu_write_image(os.fsencode(path), img.shape[1], img.shape[0], _d(img), int(ppm))
+
+    # ---- the reference's callers of the hot path (reference build only)
+    @staticmethod
+    def fit_config(lam=0.2, lr_position=0.00016, lr_scale=0.005, lr_rotation=0.001, lr_opacity=0.02,
+                   lr_color=0.0025, iters=100, seed=1, threads=1):
+        """FitConfig, include/darbs/fit_common.hpp:15-25 (its defaults)."""
+        return np.array([lam, lr_position, lr_scale, lr_rotation, lr_opacity, lr_color, iters, seed, threads],
+                        dtype=np.float64)
+
+    def read_cameras(self, path, capacity=64):
+        out = np.zeros((capacity, 22))
+        n = self.lib.darbs_cpu_read_cameras(os.fsencode(path), capacity, _d(out))
+        return n, out[:max(n, 0)]
+
+    def render_scene(self, k, psi, prims, camera, background=(0.0, 0.0, 0.0), threads=1):
+        """render_scene, fit3d.cpp:29-40 -> (status, image (h, w, 3))."""
+        prims, camera = _f64(prims), _f64(camera)
+        img = np.zeros((int(camera[5]), int(camera[4]), 3))
+        bg = np.asarray(background, dtype=np.float64)
+        st = self.lib.darbs_cpu_render_scene(C.byref(k), float(psi), prims.shape[0], _d(prims), _d(camera), _d(bg),
+                                             threads, _d(img))
+        return st, img
+
+    def fit_scene(self, k, psi, init_prims, cameras22, targets, cfg):
+        """fit_scene, fit3d.cpp:42-203.  targets: list of (h, w, 3) images, one per camera."""
+        init_prims, cameras22 = _f64(init_prims), _f64(cameras22).reshape(-1, 22)
+        n, nv, iters = init_prims.shape[0], cameras22.shape[0], max(int(cfg[6]), 1)
+        tg = np.concatenate([_f64(t).reshape(-1) for t in targets])
+        curves, finals = np.zeros((4, iters)), np.zeros(3)
+        pv, out = np.zeros(nv), np.zeros((n, 14))
+        st = self.lib.darbs_cpu_fit_scene(C.byref(k), float(psi), n, _d(init_prims), nv, _d(cameras22), _d(tg),
+                                          _d(_f64(cfg)), _d(curves), _d(finals), _d(pv), _d(out))
+        return st, dict(loss=curves[0], l1=curves[1], dssim=curves[2], psnr=curves[3], final_mse=finals[0],
+                        final_psnr=finals[1], final_ssim=finals[2], per_view_psnr=pv, primitives=out)
+
+    def fit_image(self, k, target, n_splats, cfg):
+        """fit_image, fit2d.cpp:45-188."""
+        target = _f64(target)
+        h, w = target.shape[:2]
+        iters = max(int(cfg[6]), 1)
+        curves, finals = np.zeros((4, iters)), np.zeros(3)
+        rendered, splats = np.zeros_like(target), np.zeros((n_splats, 9))
+        st = self.lib.darbs_cpu_fit_image(C.byref(k), w, h, _d(target), n_splats, _d(_f64(cfg)), _d(curves),
+                                          _d(finals), _d(rendered), _d(splats))
+        return st, dict(loss=curves[0], l1=curves[1], dssim=curves[2], psnr=curves[3], final_mse=finals[0],
+                        final_psnr=finals[1], final_ssim=finals[2], rendered=rendered, splats=splats)
 
     def adam_step(self, params, grads, m, v, lrs, t):
         params, grads, m, v, lrs = (_f64(a).copy() for a in (params, grads, m, v, lrs))

@@ -82,6 +82,24 @@ __global__ void __launch_bounds__(1024) mufu_kernel(float seed, float* sink) {
     if (s == 12345.678f) sink[0] = s;
 }
 
+// SM clock: one thread spins on a dependent FMA chain and reads the SM's cycle counter and the
+// nanosecond global timer on both sides (the ratio is the clock the SM ran at; the earlier
+// "one block's clock64 span over the kernel's event time" was wrong by the share of the kernel
+// that block did not run for).
+__global__ void clock_kernel(float seed, float* sink, long long* out) {
+    unsigned long long g0, g1;
+    float a = seed;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g0));
+    const long long c0 = clock64();
+#pragma unroll 1
+    for (int i = 0; i < 200000; ++i) a = fmaf(a, 0.999f, 0.001f);
+    const long long c1 = clock64();
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g1));
+    if (a == 12345.678f) sink[0] = a;
+    out[0] = c1 - c0;
+    out[1] = (long long)(g1 - g0);
+}
+
 }  // namespace
 }  // namespace darbs_b200
 
@@ -128,15 +146,15 @@ extern "C" darbs_status darbs_cuda_microbench(darbs_cuda_ctx* ctx, double out[8]
         DARBS_CUDA_TRY(ctx, cudaEventSynchronize(e1));
         DARBS_CUDA_TRY(ctx, cudaEventElapsedTime(&ms_m, e0, e1));
     }
-    DARBS_TRY(check_launch(ctx, "microbench", 12));
-    long long cyc = 0;
-    DARBS_CUDA_TRY(ctx, cudaMemcpy(&cyc, cycles, sizeof(cyc), cudaMemcpyDeviceToHost));
+    clock_kernel<<<1, 1, 0, ctx->stream>>>(1.0f, sink, cycles);  // right behind the load: boosted clocks
+    DARBS_TRY(check_launch(ctx, "microbench", 13));
+    long long cyc[2] = {0, 1};
+    DARBS_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+    DARBS_CUDA_TRY(ctx, cudaMemcpy(cyc, cycles, sizeof(cyc), cudaMemcpyDeviceToHost));
     const double n_thr = (double)blocks * threads;
     out[0] = n_thr * kIters * 32.0 / (ms_f * 1e-3);
     out[1] = n_thr * kIters * 16.0 / (ms_m * 1e-3);
-    // one block's clock64 span of the FFMA loop over the kernel's wall time: the
-    // block runs for (almost) the whole kernel, so cycles / time ~ SM clock.
-    out[2] = (double)cyc / (ms_f * 1e-3) / 1e6;
+    out[2] = cyc[1] > 0 ? 1e3 * (double)cyc[0] / (double)cyc[1] : 0.0;  // cycles per ns -> MHz
     out[3] = (double)sms;
     out[4] = n_thr * kIters * 32.0 / (ms_i * 1e-3);
     out[5] = n_thr * kIters * 32.0 / (ms_2 * 1e-3);  // packed instructions per second (x4 = FLOP/s)
