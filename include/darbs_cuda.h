@@ -110,6 +110,14 @@ DARBS_API int64_t darbs_cuda_launch_count(const darbs_cuda_ctx* ctx);
 /* 1: decisions that fall inside the FP32 guard band of a threshold are re-taken
  * in FP64 exactly as the reference takes them (default).  0: pure FP32. */
 DARBS_API darbs_status darbs_cuda_set_exact_decisions(darbs_cuda_ctx* ctx, int enabled);
+/* Deterministic reduction (default 0).  The reference's backward writes per-tile gradient buffers
+ * and reduces them in a fixed order, so its results do not depend on the thread count
+ * (src/rasterizer.cpp:159-165, :219-232; tests/test_rasterizer.cpp:260-273).  With 1 the render
+ * backward accumulates the per-block partial gradients, and the loss kernels their partial sums,
+ * as 64-bit FIXED-POINT integers (2^-36 resolution, range +-1.3e8): integer addition is
+ * associative, so the result is bitwise independent of the order in which blocks arrive and a
+ * rerun is bitwise identical.  0: float32 vector reductions (faster; equal up to summation order). */
+DARBS_API darbs_status darbs_cuda_set_deterministic(darbs_cuda_ctx* ctx, int enabled);
 
 /* ---- device memory ----------------------------------------------------------
  * For callers without a CUDA toolchain of their own (the C++ mirror's fit_scene keeps the raw
@@ -176,9 +184,13 @@ DARBS_API darbs_status darbs_cuda_forward(darbs_cuda_ctx* ctx, const darbs_kerne
 
 /* backward, src/rasterizer.cpp:147-234.  grads[9n] in SplatGrads order.  Returns
  * DARBS_CONTRACT_VIOLATION when (grad_width, grad_height, n) do not match the
- * last forward on this context (rasterizer.cpp:151-154).  The splat arrays are
- * re-read (the reference recomputes from the splats it is handed); pass all
- * four as NULL to reuse the forward call's values. */
+ * last forward on this context (rasterizer.cpp:151-154), or when `kernel` is not the
+ * kernel that forward ran with.  The resident aux (bins, per-block survivor streams,
+ * t_final, processed) already holds everything of the splats the backward needs, so the
+ * four splat arrays are part of the signature only to mirror the reference's and are NOT
+ * read: the gradients are those of the splats the matching forward call consumed
+ * (the reference, handed different splats with an old aux, would mix the two; that use is
+ * outside its contract as well, rasterizer.hpp:27-37).  Pass them as NULL. */
 DARBS_API darbs_status darbs_cuda_backward(darbs_cuda_ctx* ctx, const darbs_kernel_spec* kernel,
                                            int grad_width, int grad_height,
                                            const float* grad_image, int64_t n, const float* mu2,

@@ -292,6 +292,10 @@ darbs_status forward_device(darbs_cuda_ctx* ctx, const KParams& kp, int64_t n, c
                                     (int32_t*)ctx->processed.ptr, contributors));
     }
     ctx->have_forward = true;
+    ctx->fwd_family = kp.family;
+    ctx->fwd_lobes = kp.lobes;
+    ctx->fwd_beta = kp.beta_d;
+    ctx->fwd_xi = kp.xi_d;
     ctx->fwd_contrib = contributors;
     ctx->fwd_n = n;
     ctx->fwd_w = width;
@@ -366,7 +370,7 @@ void darbs_cuda_destroy(darbs_cuda_ctx* ctx) {
     DeviceBuffer* bufs[] = {&ctx->recs, &ctx->rects, &ctx->depth_keys, &ctx->order, &ctx->offsets,
                             &ctx->tile_keys, &ctx->tile_vals, &ctx->ranges, &ctx->streams, &ctx->stream_count, &ctx->cub_temp,
                             &ctx->counters, &ctx->t_final, &ctx->processed, &ctx->contributors,
-                            &ctx->image, &ctx->valid, &ctx->splat_grads, &ctx->grad_image, &ctx->loss_maps};
+                            &ctx->image, &ctx->valid, &ctx->splat_grads, &ctx->splat_grads_fx, &ctx->grad_image, &ctx->loss_maps};
     for (DeviceBuffer* b : bufs)
         if (b->ptr) cudaFree(b->ptr);
     for (int i = 0; i < 8; ++i) {
@@ -635,22 +639,15 @@ darbs_status darbs_cuda_backward(darbs_cuda_ctx* ctx, const darbs_kernel_spec* k
     DeviceGuard guard(ctx->device);
     KParams kp;
     DARBS_TRY(make_kparams(ctx, kernel, &kp));
+    if (kp.family != ctx->fwd_family || kp.lobes != ctx->fwd_lobes || kp.beta_d != ctx->fwd_beta ||
+        kp.xi_d != ctx->fwd_xi)
+        return fail(ctx, DARBS_CONTRACT_VIOLATION, "backward: not the kernel the forward call ran with");
     reset_stage_marks(ctx, {ST_RENDER_BWD});
     Stager st(ctx, space);
     const size_t px = (size_t)grad_width * grad_height;
     const float* d_gimg;
     DARBS_TRY(st.in(grad_image, 3 * px, &d_gimg));
-    const bool repack = mu2 || conic || opacity || rgb;
-    if (repack) {
-        if (!(mu2 && conic && opacity && rgb))
-            return fail(ctx, DARBS_INVALID_PARAMETER, "pass all four splat arrays or none");
-        const float *d_mu2, *d_conic, *d_opacity, *d_rgb;
-        DARBS_TRY(st.in(mu2, 2 * (size_t)n, &d_mu2));
-        DARBS_TRY(st.in(conic, 3 * (size_t)n, &d_conic));
-        DARBS_TRY(st.in(opacity, (size_t)n, &d_opacity));
-        DARBS_TRY(st.in(rgb, 3 * (size_t)n, &d_rgb));
-        DARBS_TRY(launch_pack(ctx, kp, n, d_mu2, d_conic, d_opacity, d_rgb));
-    }
+    (void)mu2, (void)conic, (void)opacity, (void)rgb;  // not read: see the header
     float* d_grads;
     DARBS_TRY(st.out(grads, (size_t)DARBS_GRADS_PER_SPLAT * (size_t)n, &d_grads));
     {
@@ -675,6 +672,19 @@ darbs_status darbs_cuda_realize(darbs_cuda_ctx* ctx, int64_t n, const float* raw
     DARBS_TRY(st.out(prims, 14 * (size_t)n, &d_prims));
     DARBS_TRY(launch_realize(ctx, n, d_raw, d_prims));
     return st.finish();
+}
+
+// the three loss sums as the device left them: doubles, or int64 fixed point in the deterministic mode
+static void read_loss_sums(const void* src, bool fixed_point, double out[3]) {
+    for (int i = 0; i < 3; ++i) {
+        if (fixed_point) {
+            long long v;
+            std::memcpy(&v, (const char*)src + 8 * i, 8);
+            out[i] = (double)v / kFixedScale;
+        } else {
+            std::memcpy(&out[i], (const char*)src + 8 * i, 8);
+        }
+    }
 }
 
 static darbs_status read_flags(darbs_cuda_ctx* ctx, const int* d_flags, int out[2]) {
@@ -860,6 +870,7 @@ darbs_status darbs_cuda_evaluate_view(darbs_cuda_ctx* ctx, const darbs_kernel_sp
     LossSlot& slot = ctx->loss_ring[(ctx->loss_head + ctx->loss_pending) % kLossRing];
     slot.count = target ? (double)(3 * px) : 0.0;
     slot.lambda = lambda;
+    slot.fixed_point = ctx->deterministic != 0;
     DARBS_CUDA_TRY(ctx, cudaMemcpyAsync(slot.host, d_flags, 40, cudaMemcpyDeviceToHost, ctx->stream));
     DARBS_CUDA_TRY(ctx, cudaEventRecord(slot.done, ctx->stream));
     ++ctx->loss_pending;
@@ -869,6 +880,12 @@ darbs_status darbs_cuda_evaluate_view(darbs_cuda_ctx* ctx, const darbs_kernel_sp
         while (ctx->loss_pending > 0) st_last = darbs_cuda_pop_loss(ctx, loss_out);
         return st_last;
     }
+    return DARBS_OK;
+}
+
+darbs_status darbs_cuda_set_deterministic(darbs_cuda_ctx* ctx, int enabled) {
+    CTX_OR_FAIL(ctx);
+    ctx->deterministic = enabled ? 1 : 0;
     return DARBS_OK;
 }
 
@@ -910,7 +927,8 @@ darbs_status darbs_cuda_pop_loss(darbs_cuda_ctx* ctx, double loss_out[4]) {
     --ctx->loss_pending;
     DARBS_CUDA_TRY(ctx, cudaEventSynchronize(slot.done));
     const int* flags = (const int*)slot.host;
-    const double* sums = (const double*)((const char*)slot.host + 16);
+    double sums[3];
+    read_loss_sums((const char*)slot.host + 16, slot.fixed_point, sums);
     double out[4] = {0.0, 0.0, 0.0, 0.0};
     if (slot.count > 0.0) {
         out[1] = sums[0] / slot.count;                                   // l1      loss.cpp:188
@@ -953,7 +971,8 @@ darbs_status darbs_cuda_loss_total(darbs_cuda_ctx* ctx, int width, int height, c
         DARBS_CUDA_TRY(ctx, cudaMemcpyAsync(ctx->pinned, d_sums, sizeof(double) * 3, cudaMemcpyDeviceToHost,
                                             ctx->stream));
         DARBS_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
-        const double* sums = (const double*)ctx->pinned;
+        double sums[3];
+        read_loss_sums(ctx->pinned, ctx->deterministic != 0, sums);
         const double count = (double)(3 * px);
         loss_out[1] = px ? sums[0] / count : 0.0;                      // loss.cpp:188
         loss_out[2] = px ? 0.5 * sums[2] / count : 0.0;                // loss.cpp:226-227 (sum of 1 - SSIM)

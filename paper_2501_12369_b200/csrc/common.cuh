@@ -46,6 +46,10 @@ struct KParams {
 //   v3 = { a, b, c, 0 }                          unscaled conic for the FP64 path
 static constexpr int kRecVecs = 4;
 
+// Fixed-point accumulation of the deterministic mode: value * 2^36 rounded to int64, added with
+// integer atomics (associative: the sum does not depend on the order of arrival).
+static constexpr double kFixedScale = 68719476736.0;  // 2^36
+
 // ---------------------------------------------------------------- workspace
 struct DeviceBuffer {
     void* ptr = nullptr;
@@ -64,6 +68,7 @@ struct LossSlot {
     cudaEvent_t done = nullptr;
     double count = 0.0;   // number of image values, 0 when the view had no target
     double lambda = 0.0;
+    bool fixed_point = false;  // the three sums are int64 fixed point (deterministic mode)
 };
 
 struct StageTimer {
@@ -85,6 +90,7 @@ struct darbs_cuda_ctx {
     int64_t launches = 0;
     int exact = 1;
     int timing = 0;
+    int deterministic = 0;  // fixed-point accumulation of gradients and loss sums (darbs_cuda_set_deterministic)
     int accumulate = 1;  // evaluate_view adds to param_grads (0: the next call overwrites)
     double stage_ms[8] = {0, 0, 0, 0, 0, 0, 0, 0};
 
@@ -106,6 +112,7 @@ struct darbs_cuda_ctx {
     darbs_b200::DeviceBuffer stage_out[8];
     darbs_b200::DeviceBuffer valid;        // per-primitive visibility (evaluate_view)
     darbs_b200::DeviceBuffer splat_grads;  // 12n: SplatGrads rows padded to 12 floats
+    darbs_b200::DeviceBuffer splat_grads_fx;  // 9n int64: the same sums in fixed point (deterministic mode)
     darbs_b200::DeviceBuffer grad_image;   // 3wh
     darbs_b200::DeviceBuffer loss_maps;    // 9wh: the three SSIM partial maps (loss.cu)
     void* pinned = nullptr;                // small pinned host scratch
@@ -125,6 +132,8 @@ struct darbs_cuda_ctx {
 
     // state of the last forward (the resident BlendAux)
     bool have_forward = false;
+    int fwd_family = -1, fwd_lobes = 0;  // the kernel the last forward ran with
+    double fwd_beta = 0.0, fwd_xi = 0.0;
     int64_t fwd_n = 0;
     int fwd_w = 0, fwd_h = 0;
     int tiles_x = 0, tiles_y = 0;

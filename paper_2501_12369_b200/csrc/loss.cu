@@ -83,7 +83,7 @@ __device__ __forceinline__ float2 fma2(float k, float2 p, float2 acc) {
     return __ffma2_rn(make_float2(k, k), p, acc);
 }
 
-__device__ __forceinline__ void block_sum3(float a, float b, float c, double* __restrict__ sums) {
+__device__ __forceinline__ void block_sum3(float a, float b, float c, double* __restrict__ sums, int fixed) {
     __shared__ double red[3][kLossThreads / 32];
     double d0 = a, d1 = b, d2 = c;
     for (int o = 16; o > 0; o >>= 1) {
@@ -100,7 +100,11 @@ __device__ __forceinline__ void block_sum3(float a, float b, float c, double* __
     if (threadIdx.x < 3) {
         double t = 0.0;
         for (int w = 0; w < kLossThreads / 32; ++w) t += red[threadIdx.x][w];
-        atomicAdd(sums + threadIdx.x, t);
+        if (fixed)  // deterministic mode: order-independent int64 fixed point in the same slot
+            atomicAdd(reinterpret_cast<unsigned long long*>(sums) + threadIdx.x,
+                      (unsigned long long)__double2ll_rn(t * kFixedScale));
+        else
+            atomicAdd(sums + threadIdx.x, t);
     }
 }
 
@@ -141,7 +145,7 @@ __global__ void __launch_bounds__(kLossThreads, 5)
 ssim_map_kernel(Window win, int w, int h, const float* __restrict__ image,
                 const float* __restrict__ target, float scale, int want_maps,
                 float* __restrict__ fa, float* __restrict__ fe, float* __restrict__ fd,
-                double* __restrict__ sums) {
+                double* __restrict__ sums, int fixed) {
     __shared__ float2 s_v01[kTH * kCols];  // (sum k x', sum k d')
     __shared__ float2 s_v23[kTH * kCols];  // (sum k x'^2, sum k d'^2)
     __shared__ float s_v4[kTH * kCols];    //  sum k x' d'
@@ -283,7 +287,7 @@ ssim_map_kernel(Window win, int w, int h, const float* __restrict__ image,
             store12<VEC>(fd + p, valid, od);
         }
     }
-    block_sum3(sum_abs, sum_sq, sum_dssim, sums);
+    block_sum3(sum_abs, sum_sq, sum_dssim, sums, fixed);
 }
 
 // ---------------------------------------------------------------- adjoint, interior pixels
@@ -530,10 +534,10 @@ darbs_status launch_loss(darbs_cuda_ctx* ctx, int width, int height, const float
     if (count >= (int64_t)1 << 31) return fail(ctx, DARBS_INVALID_PARAMETER, "loss_total: image too large");
     if (vec)
         ssim_map_kernel<true><<<grid, kLossThreads, 0, ctx->stream>>>(win, width, height, image, target, scale,
-                                                                      maps ? 1 : 0, fa, fe, fd, sums);
+                                                                      maps ? 1 : 0, fa, fe, fd, sums, ctx->deterministic);
     else
         ssim_map_kernel<false><<<grid, kLossThreads, 0, ctx->stream>>>(win, width, height, image, target, scale,
-                                                                       maps ? 1 : 0, fa, fe, fd, sums);
+                                                                       maps ? 1 : 0, fa, fe, fd, sums, ctx->deterministic);
     DARBS_TRY(check_launch(ctx, "ssim_map_kernel"));
     if (!grad_image) return DARBS_OK;
     if (!maps) {

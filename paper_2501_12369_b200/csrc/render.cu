@@ -875,7 +875,15 @@ __device__ __forceinline__ void bwd_visit(const KParams& kp, const float4* __res
     px.T = t_before;  // a lane that does not take the entry: alpha = 0, rcp(1) = 1 exactly
 }
 
-template <int FAM>
+// fixed-point add of the deterministic mode (common.cuh kFixedScale)
+__device__ __forceinline__ void fixed_add(long long* dst, float v) {
+    atomicAdd(reinterpret_cast<unsigned long long*>(dst),
+              (unsigned long long)__float2ll_rn(v * (float)kFixedScale));
+}
+
+// DET: the nine sums of an entry go to int64 fixed-point rows (9 per splat) instead of the padded
+// float rows — order-independent, see darbs_cuda_set_deterministic.
+template <int FAM, bool DET = false>
 __global__ void __launch_bounds__(kBwdThreads, 24 / kBwdWarps)
 render_bwd_kernel(KParams kp, const float4* __restrict__ recs, const int2* __restrict__ ranges,
                   const float4* __restrict__ streams, const int* __restrict__ stream_used, int W, int H,
@@ -1045,12 +1053,26 @@ render_bwd_kernel(KParams kp, const float4* __restrict__ recs, const int2* __res
                     // SplatGrads order d_color[3], d_opacity, d_conic_a, d_conic_b, d_conic_c, d_mu2;
                     // m = scale * (a dx^2 + 2 b dx dy + c dy^2): dm/da = scale dx^2, dm/db = 2 scale dx dy,
                     // dm/d mu = -(2A dx + B dy, B dx + 2C dy) with (A, B, C) the scaled record values.
-                    float* dst = grads + (size_t)__float_as_int(r2.w) * kSplatGradStride;
-                    atomicAdd(reinterpret_cast<float4*>(dst), make_float4(dc0, dc1, dc2, dop));
-                    atomicAdd(reinterpret_cast<float4*>(dst) + 1,
-                              make_float4(kp.scale * sxx, 2.f * kp.scale * sxy, kp.scale * syy,
-                                          -fmaf(2.f * r0.z, sx, r1.x * sy)));
-                    atomicAdd(dst + 8, -fmaf(r1.x, sx, 2.f * r0.w * sy));
+                    if constexpr (DET) {
+                        long long* dst = reinterpret_cast<long long*>(grads) +
+                                         (size_t)__float_as_int(r2.w) * DARBS_GRADS_PER_SPLAT;
+                        fixed_add(dst + 0, dc0);
+                        fixed_add(dst + 1, dc1);
+                        fixed_add(dst + 2, dc2);
+                        fixed_add(dst + 3, dop);
+                        fixed_add(dst + 4, kp.scale * sxx);
+                        fixed_add(dst + 5, 2.f * kp.scale * sxy);
+                        fixed_add(dst + 6, kp.scale * syy);
+                        fixed_add(dst + 7, -fmaf(2.f * r0.z, sx, r1.x * sy));
+                        fixed_add(dst + 8, -fmaf(r1.x, sx, 2.f * r0.w * sy));
+                    } else {
+                        float* dst = grads + (size_t)__float_as_int(r2.w) * kSplatGradStride;
+                        atomicAdd(reinterpret_cast<float4*>(dst), make_float4(dc0, dc1, dc2, dop));
+                        atomicAdd(reinterpret_cast<float4*>(dst) + 1,
+                                  make_float4(kp.scale * sxx, 2.f * kp.scale * sxy, kp.scale * syy,
+                                              -fmaf(2.f * r0.z, sx, r1.x * sy)));
+                        atomicAdd(dst + 8, -fmaf(r1.x, sx, 2.f * r0.w * sy));
+                    }
                 }
             }
             __syncwarp();
@@ -1064,6 +1086,15 @@ render_bwd_kernel(KParams kp, const float4* __restrict__ recs, const int2* __res
     }
     const unsigned nexact = __reduce_add_sync(kFull, px.nexact);
     if (lane == 0 && nexact) atomicAdd(counters + CNT_EXACT, (unsigned long long)nexact);
+}
+
+// deterministic mode: int64 fixed-point sums (9 per splat) -> the padded float rows
+__global__ void fixed_to_float_kernel(int64_t n, const long long* __restrict__ fx, float* __restrict__ padded) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n * kSplatGradStride) return;
+    const int64_t row = i / kSplatGradStride;
+    const int c = (int)(i - row * kSplatGradStride);
+    padded[i] = c < DARBS_GRADS_PER_SPLAT ? (float)((double)fx[row * DARBS_GRADS_PER_SPLAT + c] * (1.0 / kFixedScale)) : 0.f;
 }
 
 __global__ void export_grads_kernel(int64_t count, const float* __restrict__ padded, float* __restrict__ out) {
@@ -1191,19 +1222,36 @@ darbs_status launch_render_fwd(darbs_cuda_ctx* ctx, const KParams& kp, int width
 darbs_status launch_render_bwd(darbs_cuda_ctx* ctx, const KParams& kp, int width, int height,
                                const float bg[3], const float* grad_image, const float* t_final,
                                const int32_t* processed, int64_t n) {
-    const size_t bytes = sizeof(float) * kSplatGradStride * (size_t)(n > 0 ? n : 1);
+    const size_t rows = (size_t)(n > 0 ? n : 1);
+    const size_t bytes = sizeof(float) * kSplatGradStride * rows;
+    const bool det = ctx->deterministic != 0;
     DARBS_TRY(reserve(ctx, ctx->splat_grads, bytes));
-    DARBS_CUDA_TRY(ctx, cudaMemsetAsync(ctx->splat_grads.ptr, 0, bytes, ctx->stream));
+    float* sums = (float*)ctx->splat_grads.ptr;
+    if (det) {
+        const size_t fx_bytes = sizeof(long long) * DARBS_GRADS_PER_SPLAT * rows;
+        DARBS_TRY(reserve(ctx, ctx->splat_grads_fx, fx_bytes));
+        DARBS_CUDA_TRY(ctx, cudaMemsetAsync(ctx->splat_grads_fx.ptr, 0, fx_bytes, ctx->stream));
+        sums = (float*)ctx->splat_grads_fx.ptr;
+    }
     int tiles = ctx->tiles_x * ctx->tiles_y;
+    if (!det || tiles == 0 || n == 0)
+        DARBS_CUDA_TRY(ctx, cudaMemsetAsync(ctx->splat_grads.ptr, 0, bytes, ctx->stream));
     if (tiles == 0 || n == 0) return DARBS_OK;
     auto* counters = (unsigned long long*)ctx->counters.ptr;
     const float4* recs = (const float4*)ctx->recs.ptr;
     const int2* ranges = (const int2*)ctx->ranges.ptr;
     const int* used = (const int*)ctx->stream_count.ptr + (size_t)kBlocksPerTile * tiles;
-#define DARBS_LAUNCH_BWD(F)                                                                       \
-    render_bwd_kernel<F><<<tiles * (kBlocksPerTile / kBwdWarps), kBwdThreads, 0, ctx->stream>>>(                             \
+#define DARBS_LAUNCH_BWD_(F, D)                                                                   \
+    render_bwd_kernel<F, D><<<tiles * (kBlocksPerTile / kBwdWarps), kBwdThreads, 0, ctx->stream>>>(  \
         kp, recs, ranges, (const float4*)ctx->streams.ptr, used, width, height, ctx->tiles_x,     \
-        bg[0], bg[1], bg[2], grad_image, t_final, processed, (float*)ctx->splat_grads.ptr, counters)
+        bg[0], bg[1], bg[2], grad_image, t_final, processed, sums, counters)
+#define DARBS_LAUNCH_BWD(F)              \
+    do {                                 \
+        if (det)                         \
+            DARBS_LAUNCH_BWD_(F, true);  \
+        else                             \
+            DARBS_LAUNCH_BWD_(F, false); \
+    } while (0)
     switch (kp.fam) {
         case FAM_GAUSS2: DARBS_LAUNCH_BWD(FAM_GAUSS2); break;
         case FAM_HCOS2: DARBS_LAUNCH_BWD(FAM_HCOS2); break;
@@ -1213,7 +1261,15 @@ darbs_status launch_render_bwd(darbs_cuda_ctx* ctx, const KParams& kp, int width
         default: DARBS_LAUNCH_BWD(FAM_GENERIC); break;
     }
 #undef DARBS_LAUNCH_BWD
-    return check_launch(ctx, "render_bwd_kernel");
+#undef DARBS_LAUNCH_BWD_
+    DARBS_TRY(check_launch(ctx, "render_bwd_kernel"));
+    if (det) {
+        const int64_t count = n * kSplatGradStride;
+        fixed_to_float_kernel<<<(unsigned)((count + 255) / 256), 256, 0, ctx->stream>>>(
+            n, (const long long*)ctx->splat_grads_fx.ptr, (float*)ctx->splat_grads.ptr);
+        DARBS_TRY(check_launch(ctx, "fixed_to_float_kernel"));
+    }
+    return DARBS_OK;
 }
 
 // ctx->splat_grads (padded rows) -> out[9 n], the SplatGrads layout of the ABI.

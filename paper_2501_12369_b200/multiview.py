@@ -79,9 +79,16 @@ def bind_context(ctx, kernel, psi: float, cameras, targets, background=(0.0, 0.0
                  want_loss: bool = True):
     """(evaluate, adam) that run on a :class:`paper_2501_12369_b200.Context` through the C ABI.
     ``targets[v]`` may be a CUDA tensor (device-resident) or a pinned host array (DARBS_HOST);
-    ``lam`` defaults to FitConfig::lambda (include/darbs/fit_common.hpp:16)."""
+    ``lam`` defaults to FitConfig::lambda (include/darbs/fit_common.hpp:16).
+
+    The trainer mixes torch ops (``grads.zero_()``, the NCCL all-reduce) with the library's
+    kernels; both must run on ONE stream or nothing orders the all-reduce behind the last view's
+    gradient kernel.  The context is therefore bound to torch's current stream here, and again in
+    every call (the caller may have switched streams since)."""
+    ctx.use_torch_stream()
 
     def evaluate(view, params, grads):
+        ctx.use_torch_stream()
         tgt = targets[view]
         if hasattr(tgt, "is_cuda") and not tgt.is_cuda:
             tgt = tgt.numpy()
@@ -89,6 +96,7 @@ def bind_context(ctx, kernel, psi: float, cameras, targets, background=(0.0, 0.0
                                  param_grads=grads, want_loss=want_loss)
 
     def adam(params, grads, m, v, lrs, t):
+        ctx.use_torch_stream()
         ctx.adam_step(params.view(-1), grads.view(-1), m.view(-1), v.view(-1), lrs.view(-1), t)
 
     return evaluate, adam

@@ -187,7 +187,95 @@ def io_fixtures(ref):
     np.save(os.path.join(out, "scene_values.npy"), prims)
 
 
+REF_DATA = "/root/reference/proj/data"
+FIT_KERNELS = ["gaussian", "half-cosine-sq", "raised-cosine", "mod-sinc", "inv-multiquadratic"]
+
+
+def perturbed(truth, amount, seed):
+    """A seeded perturbation of the truth in the shape of tests/acceptance.cpp:391-405 (numpy's
+    generator, not std::normal_distribution: the start is stored, so only its shape matters)."""
+    rng = np.random.default_rng(seed)
+    p = truth.copy()
+    n = p.shape[0]
+    p[:, 0:3] += amount * rng.normal(size=(n, 3))
+    p[:, 3:6] *= np.exp(0.5 * amount * rng.normal(size=(n, 3)))
+    p[:, 6:10] += 0.5 * amount * rng.normal(size=(n, 4))
+    p[:, 10] = np.clip(p[:, 10] + 0.5 * amount * rng.normal(size=n), 0.02, 0.98)
+    p[:, 11:14] = np.clip(p[:, 11:14] + 0.5 * amount * rng.normal(size=(n, 3)), 0.02, 0.98)
+    return p
+
+
+def fit_fixtures(ref):
+    """The reference's own callers of the hot path — render_scene, fit_scene (src/fit3d.cpp) and
+    fit_image (src/fit2d.cpp) — on its own data files proj/data/demo_scene.txt + demo_cameras.txt.
+    Inputs are written by the reference's writers into tests/golden/fit/ (the C++ mirror reads
+    them); results go to tests/golden/fit.npz.  tests/test_gpu_fit_drivers.py runs the mirror's
+    fit_scene / fit_image / render_scene (host/fit_tool.cpp) on the same files on the GPU."""
+    out = os.path.join(HERE, "fit")
+    os.makedirs(out, exist_ok=True)
+    n, truth = ref.read_scene(os.path.join(REF_DATA, "demo_scene.txt"))
+    nc, cams = ref.read_cameras(os.path.join(REF_DATA, "demo_cameras.txt"))
+    assert n == 20 and nc == 4
+    assert ref.write_scene(os.path.join(out, "scene.txt"), truth) == 0
+    assert ref.write_cameras(os.path.join(out, "cameras.txt"), cams) == 0
+    res = {"truth": truth, "cameras": cams}
+    inits = {}
+    for amount in (0.02, 0.05):
+        inits[amount] = perturbed(truth, amount, 1)
+        assert ref.write_scene(os.path.join(out, f"init_{amount}.txt"), inits[amount]) == 0
+        res[f"init_{amount}"] = inits[amount]
+
+    for name in FIT_KERNELS:
+        k, psi = ref.preset(name), ref.default_psi(name)
+        # render (tools/main.cpp:336-351): every view of the demo scene
+        views = [ref.render_scene(k, psi, truth, cam)[1] for cam in cams]
+        res[f"{name}/render"] = np.stack(views)
+        # targets as the float32 dumps both sides read (image.cpp:61-85)
+        tdir = os.path.join(out, f"targets_{name}")
+        os.makedirs(tdir, exist_ok=True)
+        targets = [f32r(v) for v in views]
+        for v, t in enumerate(targets):
+            assert ref.write_image(os.path.join(tdir, f"view_{v}.dsfl"), t, ppm=False) == 0
+        # 50-iteration trajectory from the stored start, on the stored targets
+        st, r = ref.fit_scene(k, psi, inits[0.02], cams, targets, ref.fit_config(iters=50, seed=1))
+        assert st == 0
+        for key in ("loss", "l1", "dssim", "psnr", "per_view_psnr", "primitives"):
+            res[f"{name}/fit50/{key}"] = r[key]
+        res[f"{name}/fit50/final"] = np.array([r["final_mse"], r["final_psnr"], r["final_ssim"]])
+        # acceptance criterion 7 (tests/acceptance.cpp:419-470): 2000 iterations, self-rendered targets
+        st, r = ref.fit_scene(k, psi, inits[0.02], cams, views, ref.fit_config(iters=2000, seed=1))
+        assert st == 0
+        res[f"{name}/fit2000/final"] = np.array([r["final_mse"], r["final_psnr"], r["final_ssim"]])
+        res[f"{name}/fit2000/per_view_psnr"] = r["per_view_psnr"]
+        res[f"{name}/fit2000/loss"] = r["loss"]
+        print(f"  fit_scene {name}: 50 it {res[name + '/fit50/final'][1]:.2f} dB, 2000 it {r['final_psnr']:.2f} dB "
+              f"(min view {r['per_view_psnr'].min():.2f})", flush=True)
+    # the psi ablation of criterion 7: half-cosine-sq, perturbation 0.05, fitted with psi and with 1.0
+    k, psi = ref.preset("half-cosine-sq"), ref.default_psi("half-cosine-sq")
+    views = [ref.render_scene(k, psi, truth, cam)[1] for cam in cams]
+    for tag, psi_fit in (("calibrated", psi), ("ablated", 1.0)):
+        st, r = ref.fit_scene(k, psi_fit, inits[0.05], cams, views, ref.fit_config(iters=2000, seed=1))
+        assert st == 0
+        res[f"ablation/{tag}/final_psnr"] = np.array(r["final_psnr"])
+        print(f"  ablation {tag}: {r['final_psnr']:.2f} dB", flush=True)
+    # fit_image (fit2d.cpp:45-188; the determinism criterion runs it with n = 40, 60 iterations, seed 5):
+    # the target is view 0 of the Gaussian render
+    target = f32r(res["gaussian/render"][0])
+    assert ref.write_image(os.path.join(out, "target2d.dsfl"), target, ppm=False) == 0
+    for name in ("gaussian", "half-cosine-sq", "raised-cosine"):
+        st, r = ref.fit_image(ref.preset(name), target, 40, ref.fit_config(iters=60, seed=5))
+        assert st == 0
+        for key in ("loss", "l1", "dssim", "psnr", "splats", "rendered"):
+            res[f"{name}/fit_image/{key}"] = r[key]
+        res[f"{name}/fit_image/final"] = np.array([r["final_mse"], r["final_psnr"], r["final_ssim"]])
+        print(f"  fit_image {name}: {r['final_psnr']:.2f} dB", flush=True)
+    np.savez_compressed(os.path.join(HERE, "fit.npz"), **res)
+
+
 def main():
+    if len(sys.argv) > 1 and sys.argv[1] == "fit":  # only the drivers' fixtures
+        fit_fixtures(cpu.load("reference"))
+        return
     if not cpu.available("reference"):
         raise SystemExit("oracle/_ref/libdarbs_ref.so missing: run `make -C oracle ref` where /root/reference exists")
     ref = cpu.load("reference")
@@ -201,6 +289,7 @@ def main():
     np.savez_compressed(os.path.join(HERE, "adam.npz"), **adam_case(ref))
     np.savez_compressed(os.path.join(HERE, "loss.npz"), **loss_case(ref))
     io_fixtures(ref)
+    fit_fixtures(ref)
     total = sum(os.path.getsize(os.path.join(HERE, f)) for f in os.listdir(HERE) if f.endswith(".npz"))
     print(f"wrote golden fixtures, {total / 1024:.0f} KiB")
 

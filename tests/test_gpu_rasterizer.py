@@ -326,6 +326,37 @@ def test_backward_config1(ctx, port):
     run_backward_parity(ctx, port, "half-cosine-sq", 10000, 256, 256, 0)
 
 
+@pytest.mark.parametrize("name", ["gaussian", "raised-cosine", "custom:raised-cosine:1.0:0.6:2"])
+def test_backward_deterministic_mode_is_bitwise_repeatable(ctx, port, name):
+    """The reference's backward is bitwise independent of the thread count because it reduces
+    per-tile buffers in a fixed order (rasterizer.cpp:159-165, :219-232; test_rasterizer.cpp:260-273).
+    The GPU's float32 reductions arrive in scheduling order; the deterministic mode
+    (darbs_cuda_set_deterministic) accumulates them as 64-bit fixed point instead, so two runs are
+    bitwise equal — and still the oracle's gradients within the usual tolerance."""
+    n, w, h = 6000, 160, 120
+    k = oracle_kernel(port, name)
+    s = port.random_scene(k, n, w, h, 21)
+    g = port.random_image_grad(w, h, 5)
+    fr = port.forward(k, s, w, h, BG, threads=0, keep=True)
+    st, ref = port.backward(fr["handle"], k, g, s, threads=0)
+    port.forward_free(fr["handle"])
+    sc = scene_f32(s)
+    ctx.set_deterministic(True)
+    try:
+        runs = []
+        for _ in range(3):
+            ctx.forward(gpu_kernel_cached(name), **sc, width=w, height=h, background=BG, aux=False)
+            runs.append(ctx.backward(gpu_kernel_cached(name), f32(g), n).copy())
+    finally:
+        ctx.set_deterministic(False)
+    assert np.array_equal(runs[0], runs[1]) and np.array_equal(runs[0], runs[2])
+    assert grad_err(runs[0], ref).max() <= GRAD_TOL
+    # the default mode gives the same sums up to float32 summation order
+    ctx.forward(gpu_kernel_cached(name), **sc, width=w, height=h, background=BG, aux=False)
+    fast = ctx.backward(gpu_kernel_cached(name), f32(g), n)
+    assert grad_err(fast, runs[0].astype(np.float64)).max() <= GRAD_TOL
+
+
 def test_backward_rejects_mismatched_aux(ctx, port, darbs):
     """contract_violation, test_rasterizer.cpp:176-185."""
     k = port.preset("gaussian")
@@ -337,6 +368,10 @@ def test_backward_rejects_mismatched_aux(ctx, port, darbs):
     assert e.value.status == 4
     with pytest.raises(darbs.DarbsError) as e:
         ctx.backward(gpu_kernel_cached("gaussian"), np.zeros((32, 32, 3), np.float32), 9)
+    assert e.value.status == 4
+    # the resident aux belongs to the kernel the forward ran with (include/darbs_cuda.h)
+    with pytest.raises(darbs.DarbsError) as e:
+        ctx.backward(gpu_kernel_cached("half-cosine-sq"), np.zeros((32, 32, 3), np.float32), 10)
     assert e.value.status == 4
 
 
