@@ -692,8 +692,11 @@ inline Fit2DResult fit_image(const ImageBuffer& target, const KernelSpec& kernel
         const double extent = std::max(w, h);
         for (int i = 0; i < n_splats; ++i) {
             double* q = params.data() + std::size_t(i) * kP;
-            q[0] = ux(rng);
+            // the reference writes Vec2(ux(rng), uy(rng)) (fit2d.cpp:60): the order of the two draws is
+            // unspecified by the language; GCC, the compiler its build (and oracle/_ref) uses,
+            // evaluates the arguments right to left, and so does this mirror
             q[1] = uy(rng);
+            q[0] = ux(rng);
             q[2] = q[3] = std::log(r0);
             q[4] = uang(rng);
             q[5] = logit(0.5);
