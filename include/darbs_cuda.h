@@ -105,7 +105,7 @@ DARBS_API const char* darbs_cuda_last_error(const darbs_cuda_ctx* ctx);
 DARBS_API darbs_status darbs_cuda_set_stream(darbs_cuda_ctx* ctx, void* cuda_stream);
 DARBS_API darbs_status darbs_cuda_synchronize(darbs_cuda_ctx* ctx);
 /* Number of kernels this library has launched on the context since creation
- * (its own kernels and the CUB primitives it calls). */
+ * (all of them its own: no library kernel is called). */
 DARBS_API int64_t darbs_cuda_launch_count(const darbs_cuda_ctx* ctx);
 /* 1: decisions that fall inside the FP32 guard band of a threshold are re-taken
  * in FP64 exactly as the reference takes them (default).  0: pure FP32. */

@@ -331,6 +331,7 @@ darbs_status darbs_cuda_create(int device, darbs_cuda_ctx** out_ctx) {
     darbs_cuda_ctx* ctx = new (std::nothrow) darbs_cuda_ctx();
     if (!ctx) return fail(nullptr, DARBS_CUDA_ERROR, "out of host memory");
     ctx->device = device;
+    ctx->sm_count = prop.multiProcessorCount;
     DeviceGuard guard(device);
     e = cudaStreamCreateWithFlags(&ctx->own_stream, cudaStreamNonBlocking);
     if (e != cudaSuccess) {
@@ -367,8 +368,8 @@ void darbs_cuda_destroy(darbs_cuda_ctx* ctx) {
     if (!ctx) return;
     DeviceGuard guard(ctx->device);
     cudaStreamSynchronize(ctx->stream);
-    DeviceBuffer* bufs[] = {&ctx->recs, &ctx->rects, &ctx->depth_keys, &ctx->order, &ctx->offsets,
-                            &ctx->tile_keys, &ctx->tile_vals, &ctx->ranges, &ctx->streams, &ctx->stream_count, &ctx->cub_temp,
+    DeviceBuffer* bufs[] = {&ctx->recs, &ctx->rects, &ctx->depth_keys, &ctx->order,
+                            &ctx->tile_keys, &ctx->tile_vals, &ctx->ranges, &ctx->streams, &ctx->stream_count, &ctx->sort_ws, &ctx->tile_status,
                             &ctx->counters, &ctx->t_final, &ctx->processed, &ctx->contributors,
                             &ctx->image, &ctx->valid, &ctx->splat_grads, &ctx->splat_grads_fx, &ctx->grad_image, &ctx->loss_maps};
     for (DeviceBuffer* b : bufs)

@@ -1,25 +1,26 @@
 // binning.cu — device restatement of darbs::bin_splats (reference
 // src/rasterizer.cpp:25-53): global stable depth order, per-splat inclusive tile
-// rectangle, per-tile depth-ordered index lists.
+// rectangle, per-tile depth-ordered index lists.  Every kernel on the path is written here or in
+// radix.cuh; no library sort or scan is called.
 //
 // Two-level sort instead of one wide (tile, depth) key:
 //   1. stable LSD radix sort of the N (depth bits, index) pairs  -> depth order
-//      (stability gives the reference's index tie-break, rasterizer.cpp:33);
-//   2. tiles touched per splat, scanned IN DEPTH ORDER (read through the order by an input
-//      iterator of the scan) -> write offsets;
-//   3. every splat emits its (tile id, index) pairs at its offset, so the K
-//      entries are already depth-ordered globally (a warp writes the entries of its 32
-//      splats as one contiguous run);
-//   4. stable radix sort of the K entries on the tile id bits only
-//      (13 bits at 1080p: two 7-bit... passes) keeps depth order inside a tile;
-//   5. tile ranges from the sorted tile ids.
+//      (stability gives the reference's index tie-break, rasterizer.cpp:33): digit histograms of
+//      the keys, then four 8-bit passes of radix.cuh;
+//   2. expand_kernel, one pass IN DEPTH ORDER: the tiles-touched counts are scanned (chained
+//      through decoupled look-back over the CTAs), every splat emits its (tile, index) pairs at
+//      its offset — the K entries are therefore depth-ordered globally, a warp writes the entries
+//      of its 32 splats as one contiguous run — and the digit histograms of the tile sort are
+//      accumulated on the way, per SPLAT (a rectangle of nx x ny tiles adds ny to nx column
+//      digits and nx to ny row digits: ~4 shared-memory atomics per splat, not 2 per entry);
+//   3. stable radix sort of the K entries on the tile only: the key is (tile row, tile column)
+//      packed, 8 + 8 bits while both fit (16 + 16 otherwise), so one pass per coordinate byte
+//      (two at every size of BASELINE.json) keeps depth order inside a tile;
+//   4. tile ranges from the sorted keys.
 // The tile rectangle is evaluated in FP64 on the float32 inputs so that
 // floor((mu -+ R)/16) is decided on exactly the values the FP64 reference sees
 // (rasterizer.cpp:40-45).
-#include <cub/cub.cuh>
-#include <thrust/iterator/counting_iterator.h>
-#include <thrust/iterator/transform_iterator.h>
-
+#include "radix.cuh"
 #include "splat.cuh"
 
 namespace darbs_b200 {
@@ -51,15 +52,6 @@ __global__ void rect_kernel(int64_t n, const float* __restrict__ mu2,
     accumulate_tile_count(cnt, k_slots);
 }
 
-// touched[] read through the depth order, so that the scan runs in depth order without a
-// gathered copy of the counts (an input iterator of the scan).
-struct TouchedInOrder {
-    const unsigned* touched;
-    const unsigned* order;
-    __host__ __device__ unsigned operator()(unsigned r) const { return touched[order[r]]; }
-};
-using TouchedIter = thrust::transform_iterator<TouchedInOrder, thrust::counting_iterator<unsigned>>;
-
 // K, the total of the per-splat tile counts (accumulated over kSlotsK addresses by the kernel
 // that made the rectangles), goes to the device scalars and straight into pinned host memory
 // (mapped under UVA): the host needs it to size the tile sort, and a write from the SM does not
@@ -77,68 +69,167 @@ __global__ void total_kernel(const unsigned long long* __restrict__ k_slots, Sca
 }
 static_assert(kSlotsK == 64, "total_kernel sums two slots per lane");
 
-// TileKey: unsigned short while the tile ids fit 16 bits (every size of BASELINE.json does; 4K has
-// 32 400 tiles), unsigned otherwise.  The tile sort then moves 6 bytes per entry and pass, not 8.
+// TileKey: (tile row << 8 | tile column) in an unsigned short while both coordinates fit a byte
+// (every size of BASELINE.json: 120 x 68 tiles at 1080p, 240 x 135 at 4K), (row << 16 | column) in
+// an unsigned otherwise.  A tile-sort pass then moves 6 bytes per entry, not 8.
 template <typename TileKey>
-__global__ void __launch_bounds__(256)
-duplicate_kernel(int64_t n, const unsigned* __restrict__ order, const unsigned* __restrict__ offsets,
-                 const uint2* __restrict__ rects, const unsigned* __restrict__ touched, int tiles_x,
-                 TileKey* __restrict__ tile_keys, unsigned* __restrict__ tile_vals) {
-    // A warp takes 32 consecutive depth ranks and writes their entries TOGETHER: lane l owns the
-    // splat of rank r0 + l, but entry e of the warp's run is written by lane e mod 32, which
-    // finds the owning splat by a binary search over the lanes' offsets.  The writes of a warp
-    // are then one contiguous run instead of 32 interleaved short ones (rasterizer.cpp:46-50).
+struct TilePack {
+    static constexpr int kRowShift = sizeof(TileKey) == 2 ? 8 : 16;
+    static constexpr unsigned kColMask = (1u << kRowShift) - 1u;
+    __host__ __device__ static TileKey pack(unsigned tx, unsigned ty) { return (TileKey)((ty << kRowShift) | tx); }
+    __host__ __device__ static unsigned tile_of(TileKey k, int tiles_x) {
+        return ((unsigned)k >> kRowShift) * (unsigned)tiles_x + ((unsigned)k & kColMask);
+    }
+};
+
+constexpr int kExpandThreads = 256, kExpandItems = 4;
+constexpr int kExpandChunk = kExpandThreads * kExpandItems;  // depth ranks per CTA
+
+// Step 2 of the header.  status[chunks] and ticket zeroed; hist = the tile sort's digit histograms
+// [pass][256], zeroed.  plan.passes may be 0 (a single tile).
+template <typename TileKey>
+__global__ void __launch_bounds__(kExpandThreads)
+expand_kernel(unsigned n, const unsigned* __restrict__ order, const uint2* __restrict__ rects,
+              const unsigned* __restrict__ touched, radix::Plan plan, unsigned* __restrict__ hist,
+              unsigned* __restrict__ status, unsigned* __restrict__ ticket, TileKey* __restrict__ tile_keys,
+              unsigned* __restrict__ tile_vals) {
+    using Pack = TilePack<TileKey>;
+    __shared__ unsigned s_hist[radix::kMaxPasses * radix::kBins];
+    __shared__ unsigned s_wtot[kExpandThreads / 32];
+    __shared__ unsigned s_chunk, s_base;
     const unsigned full = 0xffffffffu;
-    const int lane = threadIdx.x & 31;
-    const int64_t r0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) - lane;
-    if (r0 >= n) return;
-    const int64_t r = r0 + lane;
-    unsigned idx = 0, cnt = 0, off = 0;
-    uint2 rect = make_uint2(0, 0);
-    if (r < n) {
-        idx = order[r];
-        rect = rects[idx];
-        cnt = touched[idx];
-        off = offsets[r];
-    }
-    const unsigned base = __shfl_sync(full, off, 0);
-    // lanes past n inherit the end of the run, so that the search never lands on them
-    const int last = (int)min((int64_t)31, n - 1 - r0);
-    const unsigned end = __shfl_sync(full, off + cnt, last);
-    const unsigned rel = (r < n ? off : end) - base;
-    const unsigned total = end - base;
-    for (unsigned e0 = 0; e0 < total; e0 += 32) {  // warp-uniform trip count: the shuffles need every lane
-        const unsigned e = e0 + lane;
-        int lo = 0;  // largest lane whose offset is <= e (zero-count lanes share the offset of the next)
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (tid == 0) s_chunk = atomicAdd(ticket, 1u);
+    for (int i = tid; i < plan.passes * radix::kBins; i += kExpandThreads) s_hist[i] = 0;
+    __syncthreads();
+    const unsigned chunk = s_chunk;
+    const unsigned first = chunk * (unsigned)kExpandChunk + (unsigned)(warp * kExpandItems * 32 + lane);
+
+    // this lane's splats: ranks first + 32 i
+    unsigned idx[kExpandItems], cnt[kExpandItems];
+    uint2 rect[kExpandItems];
 #pragma unroll
-        for (int step = 16; step > 0; step >>= 1) {
-            const unsigned probe = __shfl_sync(full, rel, min(lo + step, 31));
-            if (lo + step <= 31 && probe <= e) lo += step;
-        }
-        const unsigned o_rel = __shfl_sync(full, rel, lo);
-        const unsigned o_idx = __shfl_sync(full, idx, lo);
-        const unsigned rx = __shfl_sync(full, rect.x, lo), ry = __shfl_sync(full, rect.y, lo);
-        const unsigned x0 = rx & 0xffff, y0 = rx >> 16, w = (ry & 0xffff) - x0 + 1;
-        if (e < total) {
-            const unsigned q = e - o_rel;
-            const unsigned qy = q / w, qx = q - qy * w;
-            tile_keys[base + e] = (TileKey)((y0 + qy) * tiles_x + x0 + qx);
-            tile_vals[base + e] = o_idx;
+    for (int i = 0; i < kExpandItems; ++i) {
+        const unsigned r = first + 32u * i;
+        idx[i] = r < n ? order[r] : 0u;
+    }
+#pragma unroll
+    for (int i = 0; i < kExpandItems; ++i) {
+        const bool ok = first + 32u * i < n;
+        cnt[i] = ok ? touched[idx[i]] : 0u;
+        rect[i] = ok ? rects[idx[i]] : make_uint2(0, 0);
+    }
+    // the tile sort's digit histograms, per splat: nx column digits get ny, ny row digits get nx
+#pragma unroll
+    for (int i = 0; i < kExpandItems; ++i) {
+        if (cnt[i] == 0) continue;
+        const unsigned x0 = rect[i].x & 0xffffu, y0 = rect[i].x >> 16, x1 = rect[i].y & 0xffffu, y1 = rect[i].y >> 16;
+        const unsigned nx = x1 - x0 + 1u, ny = y1 - y0 + 1u;
+        for (int p = 0; p < plan.passes; ++p) {
+            const unsigned mask = (1u << plan.bits[p]) - 1u;
+            unsigned* h = s_hist + p * radix::kBins;
+            if (plan.shift[p] < Pack::kRowShift) {
+                for (unsigned x = x0; x <= x1; ++x) atomicAdd(&h[(x >> plan.shift[p]) & mask], ny);
+            } else {
+                const int sh = plan.shift[p] - Pack::kRowShift;
+                for (unsigned y = y0; y <= y1; ++y) atomicAdd(&h[(y >> sh) & mask], nx);
+            }
         }
     }
+
+    // scan of the counts in rank order: lanes of an item, items of a warp, warps of the CTA
+    unsigned rel[kExpandItems], item_total[kExpandItems], warp_total = 0;
+#pragma unroll
+    for (int i = 0; i < kExpandItems; ++i) {
+        unsigned inc = cnt[i];
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned t = __shfl_up_sync(full, inc, o);
+            if (lane >= o) inc += t;
+        }
+        rel[i] = inc - cnt[i];
+        item_total[i] = __shfl_sync(full, inc, 31);
+        warp_total += item_total[i];
+    }
+    if (lane == 0) s_wtot[warp] = warp_total;
+    __syncthreads();
+    unsigned warp_base = 0, cta_total = 0;
+#pragma unroll
+    for (int w = 0; w < kExpandThreads / 32; ++w) {
+        const unsigned t = s_wtot[w];
+        if (w < warp) warp_base += t;
+        cta_total += t;
+    }
+    // entries of all earlier CTAs: decoupled look-back, 32 predecessors per round trip
+    if (warp == 0) {
+        if (lane == 0) radix::st_relaxed(status + chunk, cta_total | (chunk == 0 ? radix::kInclusive : radix::kPartial));
+        unsigned excl = 0;
+        long long c = (long long)chunk - 1;
+        while (c >= 0) {
+            const long long at = c - lane;
+            const unsigned s = at >= 0 ? radix::ld_relaxed(status + at) : radix::kInclusive;
+            if (!__all_sync(full, (s >> 30) != 0u)) continue;  // someone has not published yet
+            const unsigned incl = __ballot_sync(full, (s >> 30) == 2u);
+            const int stop = incl ? __ffs(incl) - 1 : 31;
+            unsigned v = lane <= stop ? (s & radix::kValue) : 0u;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(full, v, o);
+            excl += v;
+            if (incl) break;
+            c -= 32;
+        }
+        if (lane == 0) {
+            if (chunk > 0) radix::st_relaxed(status + chunk, (excl + cta_total) | radix::kInclusive);
+            s_base = excl;
+        }
+    }
+    __syncthreads();
+    unsigned base = s_base + warp_base;
+
+    // A warp writes the entries of 32 consecutive ranks TOGETHER: entry e of the run is written by
+    // lane e mod 32, which finds the owning splat by a binary search over the lanes' offsets, so
+    // the writes are one contiguous run instead of 32 interleaved short ones (rasterizer.cpp:46-50).
+#pragma unroll
+    for (int i = 0; i < kExpandItems; ++i) {
+        const unsigned total = item_total[i];
+        // lanes past n hold count 0: their offset equals the end of the run and is never chosen
+        for (unsigned e0 = 0; e0 < total; e0 += 32) {  // warp-uniform trip count: the shuffles need every lane
+            const unsigned e = e0 + lane;
+            int lo = 0;  // largest lane whose offset is <= e (zero-count lanes share the offset of the next)
+#pragma unroll
+            for (int step = 16; step > 0; step >>= 1) {
+                const unsigned probe = __shfl_sync(full, rel[i], min(lo + step, 31));
+                if (lo + step <= 31 && probe <= e) lo += step;
+            }
+            const unsigned o_rel = __shfl_sync(full, rel[i], lo);
+            const unsigned o_idx = __shfl_sync(full, idx[i], lo);
+            const unsigned rx = __shfl_sync(full, rect[i].x, lo), ry = __shfl_sync(full, rect[i].y, lo);
+            const unsigned x0 = rx & 0xffffu, y0 = rx >> 16, w = (ry & 0xffffu) - x0 + 1u;
+            if (e < total) {
+                const unsigned q = e - o_rel;
+                const unsigned qy = q / w, qx = q - qy * w;
+                tile_keys[base + e] = Pack::pack(x0 + qx, y0 + qy);
+                tile_vals[base + e] = o_idx;
+            }
+        }
+        base += total;
+    }
+    __syncthreads();
+    for (int i = tid; i < plan.passes * radix::kBins; i += kExpandThreads)
+        if (s_hist[i]) atomicAdd(&hist[i], s_hist[i]);
 }
 
 template <typename TileKey>
-__global__ void ranges_kernel(int64_t k, const TileKey* __restrict__ sorted_tiles,
+__global__ void ranges_kernel(int64_t k, const TileKey* __restrict__ sorted_tiles, int tiles_x,
                               int2* __restrict__ ranges) {
     // eight consecutive entries per thread: one boundary test per entry against its predecessor
     constexpr int kPer = 8;
     const int64_t first = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) * kPer;
     if (first >= k) return;
-    unsigned prev = first > 0 ? (unsigned)sorted_tiles[first - 1] : 0xffffffffu;
+    unsigned prev = first > 0 ? TilePack<TileKey>::tile_of(sorted_tiles[first - 1], tiles_x) : 0xffffffffu;
     const int64_t stop = first + kPer < k ? first + kPer : k;
     for (int64_t i = first; i < stop; ++i) {
-        const unsigned t = sorted_tiles[i];
+        const unsigned t = TilePack<TileKey>::tile_of(sorted_tiles[i], tiles_x);
         if (t != prev) {
             ranges[t].x = (int)i;
             if (prev != 0xffffffffu) ranges[prev].y = (int)i;
@@ -149,13 +240,13 @@ __global__ void ranges_kernel(int64_t k, const TileKey* __restrict__ sorted_tile
 }
 
 template <typename TileKey>
-__global__ void export_keys_kernel(int64_t k, const TileKey* __restrict__ sorted_tiles,
+__global__ void export_keys_kernel(int64_t k, const TileKey* __restrict__ sorted_tiles, int tiles_x,
                                    const unsigned* __restrict__ point_list,
                                    const unsigned* __restrict__ rank_of,
                                    unsigned long long* __restrict__ keys) {
     int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i >= k) return;
-    keys[i] = ((unsigned long long)sorted_tiles[i] << 32) | rank_of[point_list[i]];
+    keys[i] = ((unsigned long long)TilePack<TileKey>::tile_of(sorted_tiles[i], tiles_x) << 32) | rank_of[point_list[i]];
 }
 
 __global__ void invert_order_kernel(int64_t n, const unsigned* __restrict__ order,
@@ -172,6 +263,33 @@ int bits_for(int tiles) {
     return b;
 }
 
+// The sort workspace ctx->sort_ws, in 32-bit words.  One memset clears all of it per call:
+//   depth sort:  tickets | digit histograms | status [4][chunks(n)][256]
+//   expand:      ticket | status [expand chunks(n)]
+//   tile sort:   tickets | digit histograms          (its status words: ctx->tile_status, sized by K)
+struct SortWorkspace {
+    unsigned *depth_tickets, *depth_hist, *depth_status;
+    unsigned *expand_ticket, *expand_status;
+    unsigned *tile_tickets, *tile_hist;
+    size_t words;
+};
+constexpr int kDepthPasses = 4;
+
+SortWorkspace sort_workspace(darbs_cuda_ctx* ctx, int64_t n) {
+    SortWorkspace w;
+    unsigned* p = (unsigned*)ctx->sort_ws.ptr;
+    const size_t nn = (size_t)(n > 0 ? n : 1);
+    w.depth_tickets = p;
+    w.depth_hist = p + radix::kTicketWords;
+    w.depth_status = w.depth_hist + radix::kHistWords;
+    w.expand_ticket = w.depth_status + (size_t)kDepthPasses * radix::chunks_of(nn) * radix::kBins;
+    w.expand_status = w.expand_ticket + 16;
+    w.tile_tickets = w.expand_status + ((nn + kExpandChunk - 1) / kExpandChunk + 15) / 16 * 16;
+    w.tile_hist = w.tile_tickets + radix::kTicketWords;
+    w.words = (size_t)(w.tile_hist + radix::kHistWords - p);
+    return w;
+}
+
 }  // namespace
 
 const int32_t* point_list_ptr(const darbs_cuda_ctx* ctx) {
@@ -181,39 +299,54 @@ const uint32_t* depth_order_ptr(const darbs_cuda_ctx* ctx) {
     return (const uint32_t*)ctx->order.ptr + (size_t)ctx->cur_order_buf * (ctx->order.bytes / 8);
 }
 
+// The digits of the tile sort: one pass per coordinate byte that can differ, columns first.
 template <typename TileKey>
-darbs_status tile_sort(darbs_cuda_ctx* ctx, int64_t n, int64_t k, int tiles, const unsigned* order,
-                       const unsigned* offsets, const uint2* rects, const unsigned* touched) {
+radix::Plan tile_plan(int tiles_x, int tiles_y) {
+    radix::Plan plan = {};
+    auto add = [&](int dim, int base) {
+        if (dim <= 1) return;  // a single column or row: the digit is constant
+        const int bits = bits_for(dim);
+        for (int lo = 0; lo < bits; lo += 8) {
+            plan.shift[plan.passes] = base + lo;
+            plan.bits[plan.passes] = bits - lo < 8 ? bits - lo : 8;
+            ++plan.passes;
+        }
+    };
+    add(tiles_x, 0);
+    add(tiles_y, TilePack<TileKey>::kRowShift);
+    return plan;
+}
+
+// Steps 2-4 of the header.  The small part of the sort workspace (tickets, histograms, the
+// expand kernel's status words) was cleared by binning_begin; the status words of the tile passes
+// depend on K and are cleared here.
+template <typename TileKey>
+darbs_status tile_sort(darbs_cuda_ctx* ctx, int64_t n, int64_t k, const unsigned* order, const uint2* rects,
+                       const unsigned* touched) {
     cudaStream_t s = ctx->stream;
-    // 3. duplicate in depth order
     DARBS_TRY(reserve(ctx, ctx->tile_keys, sizeof(unsigned) * 2 * (size_t)k));  // sized for 32-bit keys
     DARBS_TRY(reserve(ctx, ctx->tile_vals, sizeof(unsigned) * 2 * (size_t)k));
     TileKey* tk0 = (TileKey*)ctx->tile_keys.ptr;
     TileKey* tk1 = (TileKey*)((unsigned*)ctx->tile_keys.ptr + ctx->tile_keys.bytes / 8);
     unsigned* tv0 = (unsigned*)ctx->tile_vals.ptr;
     unsigned* tv1 = tv0 + ctx->tile_vals.bytes / 8;
-    duplicate_kernel<TileKey><<<grid_for(n, 256), 256, 0, s>>>(n, order, offsets, rects, touched, ctx->tiles_x, tk0,
-                                                      tv0);
-    DARBS_TRY(check_launch(ctx, "duplicate_kernel"));
+    const radix::Plan plan = tile_plan<TileKey>(ctx->tiles_x, ctx->tiles_y);
+    SortWorkspace ws = sort_workspace(ctx, n);
+    const size_t status_words = (size_t)plan.passes * radix::chunks_of((size_t)k) * radix::kBins;
+    DARBS_TRY(reserve(ctx, ctx->tile_status, sizeof(unsigned) * (status_words ? status_words : 1)));
+    if (status_words)
+        DARBS_CUDA_TRY(ctx, cudaMemsetAsync(ctx->tile_status.ptr, 0, sizeof(unsigned) * status_words, s));
 
-    // 4. stable sort on the tile bits
-    cub::DoubleBuffer<TileKey> tkeys(tk0, tk1);
-    cub::DoubleBuffer<unsigned> tvals(tv0, tv1);
-    const int tbits = bits_for(tiles);
-    size_t temp_bytes = 0;
-    DARBS_CUDA_TRY(ctx, cub::DeviceRadixSort::SortPairs(nullptr, temp_bytes, tkeys, tvals, (int)k, 0,
-                                                       tbits, s));
-    DARBS_TRY(reserve(ctx, ctx->cub_temp, temp_bytes));
-    temp_bytes = ctx->cub_temp.bytes;
-    DARBS_CUDA_TRY(ctx, cub::DeviceRadixSort::SortPairs(ctx->cub_temp.ptr, temp_bytes, tkeys, tvals,
-                                                       (int)k, 0, tbits, s));
-    ctx->launches += 1 + (tbits + 7) / 8;
-    ctx->cur_key_buf = tvals.Current() == tv0 ? 0 : 1;
-    const TileKey* sorted_tiles = tkeys.Current();
-
-    // 5. ranges
-    ranges_kernel<TileKey><<<grid_for(((int64_t)k + 7) / 8, 256), 256, 0, s>>>((int64_t)k, sorted_tiles,
-                                                            (int2*)ctx->ranges.ptr);
+    expand_kernel<TileKey><<<grid_for(n, kExpandChunk), kExpandThreads, 0, s>>>(
+        (unsigned)n, order, rects, touched, plan, ws.tile_hist, ws.expand_status, ws.expand_ticket, tk0, tv0);
+    DARBS_TRY(check_launch(ctx, "expand_kernel"));
+    DARBS_CUDA_TRY(ctx, radix::launch_passes<TileKey>(tk0, tv0, tk1, tv1, (unsigned)k, plan, ws.tile_tickets,
+                                                      ws.tile_hist, (unsigned*)ctx->tile_status.ptr, s));
+    ctx->launches += plan.passes;
+    ctx->cur_key_buf = plan.passes & 1;
+    const TileKey* sorted_tiles = ctx->cur_key_buf ? tk1 : tk0;
+    ranges_kernel<TileKey><<<grid_for(((int64_t)k + 7) / 8, 256), 256, 0, s>>>((int64_t)k, sorted_tiles, ctx->tiles_x,
+                                                                              (int2*)ctx->ranges.ptr);
     return check_launch(ctx, "ranges_kernel");
 }
 
@@ -244,7 +377,11 @@ darbs_status binning_begin(darbs_cuda_ctx* ctx, int64_t n, int width, int height
     DARBS_TRY(reserve(ctx, ctx->rects, sizeof(uint2) * nn + sizeof(unsigned) * nn));
     DARBS_TRY(reserve(ctx, ctx->depth_keys, sizeof(unsigned) * 2 * nn));
     DARBS_TRY(reserve(ctx, ctx->order, sizeof(unsigned) * 2 * nn));
-    DARBS_TRY(reserve(ctx, ctx->offsets, sizeof(unsigned) * (nn + 1)));
+    {
+        const size_t words = sort_workspace(ctx, n).words;
+        DARBS_TRY(reserve(ctx, ctx->sort_ws, sizeof(unsigned) * words));
+        DARBS_CUDA_TRY(ctx, cudaMemsetAsync(ctx->sort_ws.ptr, 0, sizeof(unsigned) * words, s));
+    }
     if (sinks) {
         sinks->rects = (uint2*)ctx->rects.ptr;
         sinks->touched = (unsigned*)(sinks->rects + nn);
@@ -276,7 +413,6 @@ darbs_status run_binning(darbs_cuda_ctx* ctx, int64_t n, const float* mu2, const
     unsigned* dk1 = dk0 + ctx->depth_keys.bytes / 8;
     unsigned* or0 = (unsigned*)ctx->order.ptr;
     unsigned* or1 = or0 + ctx->order.bytes / 8;
-    unsigned* offsets = (unsigned*)ctx->offsets.ptr;
 
     if (!rects_done) {
         rect_kernel<<<grid_for(n, 256), 256, 0, s>>>(n, mu2, conic, radius, depth, valid, ctx->tiles_x,
@@ -291,40 +427,28 @@ darbs_status run_binning(darbs_cuda_ctx* ctx, int64_t n, const float* mu2, const
     DARBS_TRY(check_launch(ctx, "total_kernel"));
     DARBS_CUDA_TRY(ctx, cudaEventRecord(ctx->k_ready, s));
 
-    // 1. stable depth sort
-    cub::DoubleBuffer<unsigned> dkeys(dk0, dk1);
-    cub::DoubleBuffer<unsigned> dvals(or0, or1);
-    size_t temp_bytes = 0;
-    DARBS_CUDA_TRY(ctx, cub::DeviceRadixSort::SortPairs(nullptr, temp_bytes, dkeys, dvals, (int)n, 0,
-                                                       32, s));
-    size_t scan_bytes = 0;
-    DARBS_CUDA_TRY(ctx, cub::DeviceScan::ExclusiveSum(nullptr, scan_bytes, TouchedIter(thrust::counting_iterator<unsigned>(0u), TouchedInOrder{nullptr, nullptr}),
-                                                     offsets, (int)n, s));
-    DARBS_TRY(reserve(ctx, ctx->cub_temp, temp_bytes > scan_bytes ? temp_bytes : scan_bytes));
-    temp_bytes = ctx->cub_temp.bytes;
-    DARBS_CUDA_TRY(ctx, cub::DeviceRadixSort::SortPairs(ctx->cub_temp.ptr, temp_bytes, dkeys, dvals,
-                                                       (int)n, 0, 32, s));
-    ctx->launches += 5;  // onesweep: histogram + 4 digit passes
-    const unsigned* order = dvals.Current();
-    ctx->cur_order_buf = order == or0 ? 0 : 1;
+    // 1. stable depth sort: digit histograms of the keys, then four 8-bit passes
+    const SortWorkspace ws = sort_workspace(ctx, n);
+    const radix::Plan depth_plan = {kDepthPasses, {0, 8, 16, 24}, {8, 8, 8, 8}};
+    DARBS_CUDA_TRY(ctx, radix::launch_histogram<unsigned>(dk0, (unsigned)n, depth_plan, ws.depth_hist, ctx->sm_count, s));
+    DARBS_CUDA_TRY(ctx, radix::launch_passes<unsigned>(dk0, or0, dk1, or1, (unsigned)n, depth_plan, ws.depth_tickets,
+                                                       ws.depth_hist, ws.depth_status, s));
+    ctx->launches += 1 + kDepthPasses;
+    ctx->cur_order_buf = kDepthPasses & 1;
+    const unsigned* order = ctx->cur_order_buf ? or1 : or0;
 
-    // 2. offsets in depth order, total K
-    TouchedIter in_order(thrust::counting_iterator<unsigned>(0u), TouchedInOrder{touched, order});
-    scan_bytes = ctx->cub_temp.bytes;
-    DARBS_CUDA_TRY(ctx, cub::DeviceScan::ExclusiveSum(ctx->cub_temp.ptr, scan_bytes, in_order, offsets, (int)n, s));
-    ctx->launches += 2;
-    // the host waits for K only (published before the depth sort): the GPU still has the sort and
-    // the scan queued, so it does not idle while the rest of the iteration is being launched
+    // the host waits for K only (published before the depth sort): the GPU still has the sort
+    // queued, so it does not idle while the rest of the iteration is being launched
     DARBS_CUDA_TRY(ctx, cudaEventSynchronize(ctx->k_ready));
     const unsigned long long k = *(volatile unsigned long long*)ctx->pinned;
-    if (k >= (1ull << 31)) return fail(ctx, DARBS_INVALID_PARAMETER, "more than 2^31 tile entries");
+    if (k >= (1ull << 30)) return fail(ctx, DARBS_INVALID_PARAMETER, "more than 2^30 tile entries");
     ctx->fwd_entries = (int64_t)k;
     if (k == 0) return DARBS_OK;
 
-    // 3.-5. duplicate in depth order, stable sort on the tile bits, ranges
-    if (tiles <= 65536)
-        return tile_sort<unsigned short>(ctx, n, (int64_t)k, tiles, order, offsets, rects, touched);
-    return tile_sort<unsigned>(ctx, n, (int64_t)k, tiles, order, offsets, rects, touched);
+    // 2.-4. entries in depth order, stable sort on the tile, ranges
+    if (ctx->tiles_x <= 256 && ctx->tiles_y <= 256)
+        return tile_sort<unsigned short>(ctx, n, (int64_t)k, order, rects, touched);
+    return tile_sort<unsigned>(ctx, n, (int64_t)k, order, rects, touched);
 }
 
 darbs_status export_bins(darbs_cuda_ctx* ctx, int64_t n, int32_t* tile_ranges, int32_t* point_list,
@@ -348,13 +472,13 @@ darbs_status export_bins(darbs_cuda_ctx* ctx, int64_t n, int32_t* tile_ranges, i
         invert_order_kernel<<<grid_for(n, 256), 256, 0, s>>>(n, depth_order_ptr(ctx), rank_of);
         DARBS_TRY(check_launch(ctx, "invert_order_kernel"));
         const unsigned* half = (const unsigned*)ctx->tile_keys.ptr + (size_t)ctx->cur_key_buf * (ctx->tile_keys.bytes / 8);
-        if (tiles <= 65536)
+        if (ctx->tiles_x <= 256 && ctx->tiles_y <= 256)
             export_keys_kernel<unsigned short><<<grid_for(k, 256), 256, 0, s>>>(
-                k, (const unsigned short*)half, (const unsigned*)point_list_ptr(ctx), rank_of,
+                k, (const unsigned short*)half, ctx->tiles_x, (const unsigned*)point_list_ptr(ctx), rank_of,
                 (unsigned long long*)sort_keys);
         else
             export_keys_kernel<unsigned><<<grid_for(k, 256), 256, 0, s>>>(
-                k, half, (const unsigned*)point_list_ptr(ctx), rank_of, (unsigned long long*)sort_keys);
+                k, half, ctx->tiles_x, (const unsigned*)point_list_ptr(ctx), rank_of, (unsigned long long*)sort_keys);
         DARBS_TRY(check_launch(ctx, "export_keys_kernel"));
     }
     return DARBS_OK;

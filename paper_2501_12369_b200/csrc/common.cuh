@@ -80,6 +80,7 @@ struct StageTimer {
 
 struct darbs_cuda_ctx {
     int device = 0;
+    int sm_count = 148;
     cudaStream_t own_stream = nullptr;
     cudaStream_t stream = nullptr;
     // host -> device uploads that a call does not need until late (the target image of
@@ -99,13 +100,13 @@ struct darbs_cuda_ctx {
     darbs_b200::DeviceBuffer rects;        // n * uint2 (packed tile rect, tiles touched)
     darbs_b200::DeviceBuffer depth_keys;   // 2 * n u32 (double buffer)
     darbs_b200::DeviceBuffer order;        // 2 * n u32 (double buffer)
-    darbs_b200::DeviceBuffer offsets;      // n u32 exclusive scan (+1)
     darbs_b200::DeviceBuffer tile_keys;    // 2 * K u32
     darbs_b200::DeviceBuffer tile_vals;    // 2 * K u32
     darbs_b200::DeviceBuffer ranges;       // tiles * int2
     darbs_b200::DeviceBuffer streams;      // 8 (K + 32 tiles) x 48 B: per-block survivor streams (render.cu)
     darbs_b200::DeviceBuffer stream_count; // 2 x 8 tiles int: entries per stream | entries the forward composited
-    darbs_b200::DeviceBuffer cub_temp;
+    darbs_b200::DeviceBuffer sort_ws;      // tickets, digit histograms and status words of the sorts (binning.cu)
+    darbs_b200::DeviceBuffer tile_status;  // status words of the tile sort's passes (sized by K)
     darbs_b200::DeviceBuffer counters;     // Counters + scalars
     darbs_b200::DeviceBuffer t_final, processed, contributors, image;  // per-pixel aux
     darbs_b200::DeviceBuffer stage_in[8];  // staging for DARBS_HOST calls / internal SoA

@@ -693,7 +693,7 @@ inline Fit2DResult fit_image(const ImageBuffer& target, const KernelSpec& kernel
         for (int i = 0; i < n_splats; ++i) {
             double* q = params.data() + std::size_t(i) * kP;
             // the reference writes Vec2(ux(rng), uy(rng)) (fit2d.cpp:60): the order of the two draws is
-            // unspecified by the language; GCC, the compiler its build (and oracle/_ref) uses,
+            // unspecified by the language; GCC, the compiler the reference is built with,
             // evaluates the arguments right to left, and so does this mirror
             q[1] = uy(rng);
             q[0] = ux(rng);
