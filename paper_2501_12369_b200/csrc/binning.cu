@@ -56,16 +56,22 @@ __global__ void rect_kernel(int64_t n, const float* __restrict__ mu2,
 // that made the rectangles), goes to the device scalars and straight into pinned host memory
 // (mapped under UVA): the host needs it to size the tile sort, and a write from the SM does not
 // queue behind a bulk host <-> device copy that may be in flight on the copy engines.  It is
-// known before the depth sort starts, so the host reads it while the GPU sorts.
-__global__ void total_kernel(const unsigned long long* __restrict__ k_slots, Scalars* __restrict__ scalars,
-                             volatile unsigned long long* host_total) {
-    unsigned long long k = k_slots[threadIdx.x] + k_slots[threadIdx.x + 32];
-    for (int o = 16; o > 0; o >>= 1) k += __shfl_xor_sync(0xffffffffu, k, o);
-    if (threadIdx.x == 0) {
-        scalars->total_entries = k;
-        *host_total = k;
-        __threadfence_system();
+// known before the depth sort starts, so the host reads it while the GPU sorts.  The kernel that
+// counts the depth keys' digit histograms (the first of the sort) does it on the side.
+__global__ void __launch_bounds__(radix::kHistogramThreads)
+depth_histogram_kernel(const unsigned* __restrict__ keys, unsigned n, radix::Plan plan, unsigned* __restrict__ hist,
+                       const unsigned long long* __restrict__ k_slots, Scalars* __restrict__ scalars,
+                       volatile unsigned long long* host_total) {
+    if (blockIdx.x == 0 && threadIdx.x < 32) {
+        unsigned long long k = k_slots[threadIdx.x] + k_slots[threadIdx.x + 32];
+        for (int o = 16; o > 0; o >>= 1) k += __shfl_xor_sync(0xffffffffu, k, o);
+        if (threadIdx.x == 0) {
+            scalars->total_entries = k;
+            *host_total = k;
+            __threadfence_system();
+        }
     }
+    radix::histogram_body<unsigned, radix::kHistogramThreads>(keys, n, plan, hist);
 }
 static_assert(kSlotsK == 64, "total_kernel sums two slots per lane");
 
@@ -82,12 +88,12 @@ struct TilePack {
     }
 };
 
-constexpr int kExpandThreads = 256, kExpandItems = 4;
+constexpr int kExpandThreads = 256, kExpandItems = 8;
 constexpr int kExpandChunk = kExpandThreads * kExpandItems;  // depth ranks per CTA
 
 // Step 2 of the header.  status[chunks] and ticket zeroed; hist = the tile sort's digit histograms
 // [pass][256], zeroed.  plan.passes may be 0 (a single tile).
-template <typename TileKey>
+template <typename TileKey, bool BYTE_DIGITS>
 __global__ void __launch_bounds__(kExpandThreads)
 expand_kernel(unsigned n, const unsigned* __restrict__ order, const uint2* __restrict__ rects,
               const unsigned* __restrict__ touched, radix::Plan plan, unsigned* __restrict__ hist,
@@ -119,24 +125,6 @@ expand_kernel(unsigned n, const unsigned* __restrict__ order, const uint2* __res
         cnt[i] = ok ? touched[idx[i]] : 0u;
         rect[i] = ok ? rects[idx[i]] : make_uint2(0, 0);
     }
-    // the tile sort's digit histograms, per splat: nx column digits get ny, ny row digits get nx
-#pragma unroll
-    for (int i = 0; i < kExpandItems; ++i) {
-        if (cnt[i] == 0) continue;
-        const unsigned x0 = rect[i].x & 0xffffu, y0 = rect[i].x >> 16, x1 = rect[i].y & 0xffffu, y1 = rect[i].y >> 16;
-        const unsigned nx = x1 - x0 + 1u, ny = y1 - y0 + 1u;
-        for (int p = 0; p < plan.passes; ++p) {
-            const unsigned mask = (1u << plan.bits[p]) - 1u;
-            unsigned* h = s_hist + p * radix::kBins;
-            if (plan.shift[p] < Pack::kRowShift) {
-                for (unsigned x = x0; x <= x1; ++x) atomicAdd(&h[(x >> plan.shift[p]) & mask], ny);
-            } else {
-                const int sh = plan.shift[p] - Pack::kRowShift;
-                for (unsigned y = y0; y <= y1; ++y) atomicAdd(&h[(y >> sh) & mask], nx);
-            }
-        }
-    }
-
     // scan of the counts in rank order: lanes of an item, items of a warp, warps of the CTA
     unsigned rel[kExpandItems], item_total[kExpandItems], warp_total = 0;
 #pragma unroll
@@ -160,9 +148,38 @@ expand_kernel(unsigned n, const unsigned* __restrict__ order, const uint2* __res
         if (w < warp) warp_base += t;
         cta_total += t;
     }
+    if (tid == 0) radix::st_relaxed(status + chunk, cta_total | (chunk == 0 ? radix::kInclusive : radix::kPartial));
+    // the tile sort's digit histograms, per splat: nx column digits get ny, ny row digits get nx
+    // (after the publish: this work runs under the look-back of the CTAs behind this one)
+    if (BYTE_DIGITS) {  // pass 0 = the column, pass 1 = the row: no shifts, no masks
+#pragma unroll
+        for (int i = 0; i < kExpandItems; ++i) {
+            if (cnt[i] == 0) continue;
+            const unsigned x0 = rect[i].x & 0xffffu, y0 = rect[i].x >> 16, x1 = rect[i].y & 0xffffu, y1 = rect[i].y >> 16;
+            const unsigned nx = x1 - x0 + 1u, ny = y1 - y0 + 1u;
+            for (unsigned x = x0; x <= x1; ++x) atomicAdd(&s_hist[x], ny);
+            for (unsigned y = y0; y <= y1; ++y) atomicAdd(&s_hist[radix::kBins + y], nx);
+        }
+    } else {
+#pragma unroll
+        for (int i = 0; i < kExpandItems; ++i) {
+            if (cnt[i] == 0) continue;
+            const unsigned x0 = rect[i].x & 0xffffu, y0 = rect[i].x >> 16, x1 = rect[i].y & 0xffffu, y1 = rect[i].y >> 16;
+            const unsigned nx = x1 - x0 + 1u, ny = y1 - y0 + 1u;
+            for (int p = 0; p < plan.passes; ++p) {
+                const unsigned mask = (1u << plan.bits[p]) - 1u;
+                unsigned* h = s_hist + p * radix::kBins;
+                if (plan.shift[p] < Pack::kRowShift) {
+                    for (unsigned x = x0; x <= x1; ++x) atomicAdd(&h[(x >> plan.shift[p]) & mask], ny);
+                } else {
+                    const int sh = plan.shift[p] - Pack::kRowShift;
+                    for (unsigned y = y0; y <= y1; ++y) atomicAdd(&h[(y >> sh) & mask], nx);
+                }
+            }
+        }
+    }
     // entries of all earlier CTAs: decoupled look-back, 32 predecessors per round trip
     if (warp == 0) {
-        if (lane == 0) radix::st_relaxed(status + chunk, cta_total | (chunk == 0 ? radix::kInclusive : radix::kPartial));
         unsigned excl = 0;
         long long c = (long long)chunk - 1;
         while (c >= 0) {
@@ -337,8 +354,14 @@ darbs_status tile_sort(darbs_cuda_ctx* ctx, int64_t n, int64_t k, const unsigned
     if (status_words)
         DARBS_CUDA_TRY(ctx, cudaMemsetAsync(ctx->tile_status.ptr, 0, sizeof(unsigned) * status_words, s));
 
-    expand_kernel<TileKey><<<grid_for(n, kExpandChunk), kExpandThreads, 0, s>>>(
-        (unsigned)n, order, rects, touched, plan, ws.tile_hist, ws.expand_status, ws.expand_ticket, tk0, tv0);
+    // pass 0 = the column byte, pass 1 = the row byte: the histograms need neither shifts nor masks
+    const bool byte_digits = sizeof(TileKey) == 2 && plan.passes == 2 && plan.shift[1] == 8;
+    if (byte_digits)
+        expand_kernel<TileKey, true><<<grid_for(n, kExpandChunk), kExpandThreads, 0, s>>>(
+            (unsigned)n, order, rects, touched, plan, ws.tile_hist, ws.expand_status, ws.expand_ticket, tk0, tv0);
+    else
+        expand_kernel<TileKey, false><<<grid_for(n, kExpandChunk), kExpandThreads, 0, s>>>(
+            (unsigned)n, order, rects, touched, plan, ws.tile_hist, ws.expand_status, ws.expand_ticket, tk0, tv0);
     DARBS_TRY(check_launch(ctx, "expand_kernel"));
     DARBS_CUDA_TRY(ctx, radix::launch_passes<TileKey>(tk0, tv0, tk1, tv1, (unsigned)k, plan, ws.tile_tickets,
                                                       ws.tile_hist, (unsigned*)ctx->tile_status.ptr, s));
@@ -364,9 +387,9 @@ darbs_status binning_begin(darbs_cuda_ctx* ctx, int64_t n, int width, int height
     DARBS_TRY(reserve(ctx, ctx->ranges, sizeof(int2) * (size_t)(tiles > 0 ? tiles : 1)));
     DARBS_CUDA_TRY(ctx, cudaMemsetAsync(ctx->ranges.ptr, 0, sizeof(int2) * (size_t)tiles, s));
     Scalars* scalars = (Scalars*)((unsigned long long*)ctx->counters.ptr + 8);
-    DARBS_CUDA_TRY(ctx, cudaMemsetAsync(ctx->counters.ptr, 0, sizeof(unsigned long long) * 10, s));
+    // work counters, scalars and the K slots in one clear (what lies between them is scratch)
     unsigned long long* k_slots = (unsigned long long*)ctx->counters.ptr + kSlotsKBase;
-    DARBS_CUDA_TRY(ctx, cudaMemsetAsync(k_slots, 0, sizeof(unsigned long long) * kSlotsK, s));
+    DARBS_CUDA_TRY(ctx, cudaMemsetAsync(ctx->counters.ptr, 0, sizeof(unsigned long long) * (kSlotsKBase + kSlotsK), s));
     ctx->fwd_entries = 0;
     ctx->cur_key_buf = 0;
     ctx->cur_order_buf = 0;
@@ -420,20 +443,19 @@ darbs_status run_binning(darbs_cuda_ctx* ctx, int64_t n, const float* mu2, const
                                                      (unsigned long long*)ctx->counters.ptr + kSlotsKBase);
         DARBS_TRY(check_launch(ctx, "rect_kernel"));
     }
-    // K is complete: publish it now, and let the host pick it up while the depth sort runs
+    // 1. stable depth sort: digit histograms of the keys, then four 8-bit passes.  K is complete:
+    // the histogram kernel publishes it, and the host picks it up while the depth sort runs
     DARBS_TRY(reserve_pinned(ctx, 64));
-    total_kernel<<<1, 32, 0, s>>>((const unsigned long long*)ctx->counters.ptr + kSlotsKBase, scalars,
-                                  (volatile unsigned long long*)ctx->pinned);
-    DARBS_TRY(check_launch(ctx, "total_kernel"));
-    DARBS_CUDA_TRY(ctx, cudaEventRecord(ctx->k_ready, s));
-
-    // 1. stable depth sort: digit histograms of the keys, then four 8-bit passes
     const SortWorkspace ws = sort_workspace(ctx, n);
     const radix::Plan depth_plan = {kDepthPasses, {0, 8, 16, 24}, {8, 8, 8, 8}};
-    DARBS_CUDA_TRY(ctx, radix::launch_histogram<unsigned>(dk0, (unsigned)n, depth_plan, ws.depth_hist, ctx->sm_count, s));
+    depth_histogram_kernel<<<radix::histogram_blocks((unsigned)n, ctx->sm_count), radix::kHistogramThreads, 0, s>>>(
+        dk0, (unsigned)n, depth_plan, ws.depth_hist, (const unsigned long long*)ctx->counters.ptr + kSlotsKBase, scalars,
+        (volatile unsigned long long*)ctx->pinned);
+    DARBS_TRY(check_launch(ctx, "depth_histogram_kernel"));
+    DARBS_CUDA_TRY(ctx, cudaEventRecord(ctx->k_ready, s));
     DARBS_CUDA_TRY(ctx, radix::launch_passes<unsigned>(dk0, or0, dk1, or1, (unsigned)n, depth_plan, ws.depth_tickets,
                                                        ws.depth_hist, ws.depth_status, s));
-    ctx->launches += 1 + kDepthPasses;
+    ctx->launches += kDepthPasses;
     ctx->cur_order_buf = kDepthPasses & 1;
     const unsigned* order = ctx->cur_order_buf ? or1 : or0;
 

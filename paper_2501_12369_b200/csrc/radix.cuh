@@ -89,8 +89,8 @@ __device__ __forceinline__ uint2 scan_bins2(unsigned a, unsigned b, uint2* ws) {
 
 // ---------------------------------------------------------------- digit histograms of all passes
 template <typename KeyT, int THREADS>
-__global__ void __launch_bounds__(THREADS)
-histogram_kernel(const KeyT* __restrict__ keys, unsigned n, Plan plan, unsigned* __restrict__ hist) {
+__device__ __forceinline__ void histogram_body(const KeyT* __restrict__ keys, unsigned n, const Plan& plan,
+                                               unsigned* __restrict__ hist) {
     __shared__ unsigned sh[kMaxPasses * kBins];
     for (int i = threadIdx.x; i < kMaxPasses * kBins; i += THREADS) sh[i] = 0;
     __syncthreads();
@@ -119,6 +119,18 @@ histogram_kernel(const KeyT* __restrict__ keys, unsigned n, Plan plan, unsigned*
     __syncthreads();
     for (int i = threadIdx.x; i < plan.passes * kBins; i += THREADS)
         if (sh[i]) atomicAdd(&hist[i], sh[i]);
+}
+
+template <typename KeyT, int THREADS>
+__global__ void __launch_bounds__(THREADS)
+histogram_kernel(const KeyT* __restrict__ keys, unsigned n, Plan plan, unsigned* __restrict__ hist) {
+    histogram_body<KeyT, THREADS>(keys, n, plan, hist);
+}
+
+constexpr int kHistogramThreads = 512;
+inline unsigned histogram_blocks(unsigned n, int sms) {
+    unsigned blocks = (n + kHistogramThreads * 16 - 1) / (kHistogramThreads * 16);
+    return blocks > (unsigned)(4 * sms) ? (unsigned)(4 * sms) : blocks;
 }
 
 // ---------------------------------------------------------------- one pass
@@ -349,10 +361,7 @@ template <typename KeyT>
 inline cudaError_t launch_histogram(const KeyT* keys, unsigned n, const Plan& plan, unsigned* hist, int sms,
                                     cudaStream_t stream) {
     if (n == 0) return cudaSuccess;
-    constexpr int kT = 512;
-    unsigned blocks = (n + kT * 16 - 1) / (kT * 16);
-    if (blocks > (unsigned)(4 * sms)) blocks = 4 * sms;
-    histogram_kernel<KeyT, kT><<<blocks, kT, 0, stream>>>(keys, n, plan, hist);
+    histogram_kernel<KeyT, kHistogramThreads><<<histogram_blocks(n, sms), kHistogramThreads, 0, stream>>>(keys, n, plan, hist);
     return cudaGetLastError();
 }
 
