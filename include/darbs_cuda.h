@@ -292,6 +292,38 @@ DARBS_API darbs_status darbs_cuda_adam_step(darbs_cuda_ctx* ctx, int64_t dim, fl
                                             const float* grads, float* m, float* v,
                                             const float* lrs, int t, darbs_space space);
 
+/* ---- multi-GPU: view-parallel training iteration ------------------------------
+ * fit_scene's iteration, src/fit3d.cpp:104-184, with the view loop sharded over the ranks of one
+ * node (one process and one context per GPU; view v belongs to rank v mod world).
+ * Every rank keeps a replica of params / m / v; the only exchange on the path is ONE all-reduce
+ * (sum, no 1/V scaling: the reference sums, fit3d.cpp:148-158) of the 14 n float32 gradient
+ * buffer per iteration, over NCCL (NVLink / NVSwitch), issued on its own stream in pieces so
+ * that Adam updates a piece while the next is still being reduced.  NCCL is bound at run time
+ * (dlopen libnccl.so.2; the environment variable DARBS_NCCL_LIB overrides the name), so the
+ * single-GPU entry points have no dependency on it.  Without a communicator (or world == 1)
+ * darbs_cuda_train_step is the plain single-GPU iteration. */
+typedef struct { char bytes[128]; } darbs_comm_id;   /* ncclUniqueId */
+/* Rank 0 makes the id and hands it to the other ranks by any means (file, socket, MPI). */
+DARBS_API darbs_status darbs_cuda_comm_unique_id(darbs_comm_id* out);
+/* Collective over all ranks (ncclCommInitRank).  Replaces an existing communicator. */
+DARBS_API darbs_status darbs_cuda_comm_init(darbs_cuda_ctx* ctx, const darbs_comm_id* id, int rank,
+                                            int world);
+DARBS_API darbs_status darbs_cuda_comm_destroy(darbs_cuda_ctx* ctx);
+/* One iteration.  All arrays are DARBS_DEVICE: params, grads, m, v, lrs [14 n]; cameras
+ * [n_local_views][22]; targets[n_local_views] device pointers to [3wh] images of the cameras'
+ * sizes.  The rank's local views are evaluated (the first overwrites `grads`, fit3d.cpp:107),
+ * `grads` is all-reduced, Adam step `t` (1-based) is applied.  loss_out (may be NULL) receives
+ * the mean over all n_views_total views of (total, l1, dssim, mse) (fit3d.cpp:161-165; a second
+ * all-reduce of four doubles, which synchronises).  Errors of a view (all primitives culled,
+ * non-finite loss) are reported after the iteration has been queued, like darbs_cuda_pop_loss. */
+DARBS_API darbs_status darbs_cuda_train_step(darbs_cuda_ctx* ctx, const darbs_kernel_spec* kernel,
+                                             double psi, int64_t n, float* params, float* grads,
+                                             float* m, float* v, const float* lrs,
+                                             int n_local_views, const double* cameras,
+                                             const float* const* targets, double lambda,
+                                             const float background[3], int t, int n_views_total,
+                                             double loss_out[4]);
+
 /* ---- instrumentation ---------------------------------------------------------- */
 
 /* Device time in milliseconds of the stages of the last forward / backward /

@@ -10,8 +10,8 @@ There is NO CPU fallback: :mod:`paper_2501_12369_b200.api` (loaded on first use 
 below) raises if the CUDA library has not been built, and creating a context raises if no B200 is
 visible.
 """
-_API = ("DEVICE", "HOST", "Context", "DarbsError", "KernelSpec", "default_psi", "kernel_preset", "lib_path",
-        "make_kernel", "version")
+_API = ("DEVICE", "HOST", "Context", "DarbsError", "KernelSpec", "comm_unique_id", "default_psi", "kernel_preset",
+        "lib_path", "make_kernel", "version")
 
 __all__ = list(_API)
 

@@ -108,6 +108,11 @@ def _load():
     lib.darbs_cuda_download.argtypes = [vp, vp, vp, C.c_uint64]
     lib.darbs_cuda_device_zero.argtypes = [vp, vp, C.c_uint64]
     lib.darbs_cuda_set_accumulate.argtypes = [vp, i32]
+    lib.darbs_cuda_comm_unique_id.argtypes = [C.c_char_p]
+    lib.darbs_cuda_comm_init.argtypes = [vp, C.c_char_p, i32, i32]
+    lib.darbs_cuda_comm_destroy.argtypes = [vp]
+    lib.darbs_cuda_train_step.argtypes = [vp, C.POINTER(KernelSpec), dbl, i64, vp, vp, vp, vp, vp, i32, C.POINTER(dbl),
+                                          C.POINTER(vp), dbl, C.POINTER(C.c_float), i32, i32, C.POINTER(dbl)]
     lib.darbs_cuda_set_stage_timing.argtypes = [vp, i32]
     lib.darbs_cuda_stage_times.argtypes = [vp, C.POINTER(dbl)]
     lib.darbs_cuda_work_counters.argtypes = [vp, C.POINTER(i64)]
@@ -123,7 +128,8 @@ EXPORTED_SYMBOLS = (
     "darbs_cuda_backward darbs_cuda_realize darbs_cuda_project darbs_cuda_backward_projection "
     "darbs_cuda_evaluate_view darbs_cuda_prefetch_target darbs_cuda_pop_loss darbs_cuda_adam_step darbs_cuda_set_stage_timing darbs_cuda_stage_times "
     "darbs_cuda_work_counters darbs_cuda_microbench darbs_cuda_loss_total darbs_cuda_device_alloc "
-    "darbs_cuda_device_free darbs_cuda_upload darbs_cuda_download darbs_cuda_device_zero darbs_cuda_set_accumulate"
+    "darbs_cuda_device_free darbs_cuda_upload darbs_cuda_download darbs_cuda_device_zero darbs_cuda_set_accumulate "
+    "darbs_cuda_comm_unique_id darbs_cuda_comm_init darbs_cuda_comm_destroy darbs_cuda_train_step"
 ).split()
 
 
@@ -134,6 +140,15 @@ def version() -> str:
 def _raise(status: int, ctx=None):
     msg = _lib.darbs_cuda_last_error(ctx).decode()
     raise DarbsError(status, msg)
+
+
+def comm_unique_id() -> bytes:
+    """ncclGetUniqueId: rank 0 makes it and hands it to the other ranks (darbs_cuda_comm_unique_id)."""
+    buf = C.create_string_buffer(128)
+    st = _lib.darbs_cuda_comm_unique_id(buf)
+    if st != 0:
+        _raise(st)
+    return buf.raw
 
 
 def make_kernel(family, beta: float, xi: float, lobes: int = 1) -> KernelSpec:
@@ -472,6 +487,31 @@ class Context:
         loss = (C.c_double * 4)()
         self._check(_lib.darbs_cuda_loss_total(self._h, w, h, pr, pt, float(lam), loss, pg, a.space))
         return tuple(float(x) for x in loss), grad
+
+    # ------------------------------------------------------------ multi-GPU (view-parallel)
+    def comm_init(self, comm_id: bytes, rank: int, world: int):
+        """ncclCommInitRank on this context's GPU (collective over the ranks); comm_id from comm_unique_id()."""
+        self._check(_lib.darbs_cuda_comm_init(self._h, comm_id, rank, world))
+
+    def comm_destroy(self):
+        self._check(_lib.darbs_cuda_comm_destroy(self._h))
+
+    def train_step(self, kernel: KernelSpec, psi: float, params, grads, m, v, lrs, cameras, targets, lam: float,
+                   t: int, n_views_total: int, background=(0.0, 0.0, 0.0), want_loss: bool = True):
+        """One fit_scene iteration (src/fit3d.cpp:104-184) over this rank's views: evaluate, all-reduce of the
+        gradients over the communicator (if any), Adam.  All arrays are CUDA tensors; cameras: [views][22]."""
+        n = params.numel() // 14
+        cams = np.ascontiguousarray(np.asarray(cameras, dtype=np.float64).reshape(-1))
+        nv = cams.size // 22
+        assert nv == len(targets)
+        tp = (C.c_void_p * max(nv, 1))(*[C.c_void_p(tt.data_ptr()) for tt in targets])
+        bg = (C.c_float * 3)(*[float(x) for x in background])
+        loss = (C.c_double * 4)()
+        ptr = lambda a: C.c_void_p(a.data_ptr())  # noqa: E731
+        self._check(_lib.darbs_cuda_train_step(self._h, C.byref(kernel), psi, n, ptr(params), ptr(grads), ptr(m), ptr(v),
+                                               ptr(lrs), nv, cams.ctypes.data_as(C.POINTER(C.c_double)), tp, lam, bg, t,
+                                               n_views_total, loss if want_loss else None))
+        return tuple(float(x) for x in loss) if want_loss else None
 
     def adam_step(self, params, grads, m, v, lrs, t: int):
         """adam_step, include/darbs/optim.hpp:24-39 (in place)."""

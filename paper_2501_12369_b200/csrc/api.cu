@@ -368,6 +368,7 @@ void darbs_cuda_destroy(darbs_cuda_ctx* ctx) {
     if (!ctx) return;
     DeviceGuard guard(ctx->device);
     cudaStreamSynchronize(ctx->stream);
+    destroy_comm(ctx);
     DeviceBuffer* bufs[] = {&ctx->recs, &ctx->rects, &ctx->depth_keys, &ctx->order,
                             &ctx->tile_keys, &ctx->tile_vals, &ctx->ranges, &ctx->streams, &ctx->stream_count, &ctx->sort_ws, &ctx->tile_status,
                             &ctx->counters, &ctx->t_final, &ctx->processed, &ctx->contributors,

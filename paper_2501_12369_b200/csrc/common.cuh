@@ -145,6 +145,7 @@ struct darbs_cuda_ctx {
     int cur_order_buf = 0;
 
     darbs_b200::StageTimer timer;
+    void* comm = nullptr;  // darbs_b200::Comm (multigpu.cu): the NCCL communicator of darbs_cuda_comm_init
 };
 
 namespace darbs_b200 {
@@ -215,6 +216,9 @@ darbs_status export_bins(darbs_cuda_ctx* ctx, int64_t n, int32_t* tile_ranges, i
                          uint64_t* sort_keys, int32_t* depth_order);
 const int32_t* point_list_ptr(const darbs_cuda_ctx* ctx);
 const uint32_t* depth_order_ptr(const darbs_cuda_ctx* ctx);
+
+// multigpu.cu
+void destroy_comm(darbs_cuda_ctx* ctx);
 
 // geometry.cu
 struct CameraD {

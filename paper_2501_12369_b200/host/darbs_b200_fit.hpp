@@ -512,8 +512,21 @@ struct Fit3DResult {
 };
 
 // fit_scene, src/fit3d.cpp:42-203.  The loop is the reference's; the state lives on the GPU.
+// Which of the views this process owns when the fit runs on several GPUs of one node (one process
+// per GPU): view v belongs to rank v mod world.  With world > 1 the session's
+// context must hold a communicator (darbs_cuda_comm_init, collective over the ranks); gradients
+// are then summed over all ranks' views by one NCCL all-reduce per iteration inside
+// darbs_cuda_train_step, and every rank returns the same fitted scene.
+struct ViewShard {
+    int rank = 0;
+    int world = 1;
+};
+
 inline Fit3DResult fit_scene(const std::vector<View>& views, const KernelSpec& kernel, double psi,
-                             const std::vector<Primitive3D>& init, const FitConfig& config) {
+                             const std::vector<Primitive3D>& init, const FitConfig& config,
+                             const ViewShard& shard = ViewShard()) {
+    if (shard.world < 1 || shard.rank < 0 || shard.rank >= shard.world)
+        throw invalid_parameter("fit_scene: bad view shard");
     if (views.size() < 2) throw invalid_parameter("fit_scene: need at least 2 views");
     if (init.empty()) throw invalid_parameter("fit_scene: empty initial primitive set");
     const auto t0 = std::chrono::steady_clock::now();
@@ -605,11 +618,26 @@ inline Fit3DResult fit_scene(const std::vector<View>& views, const KernelSpec& k
         result.report.psnr_curve.push_back(s.mse > 0.0 ? -10.0 * std::log10(s.mse) : 99.0);
     };
     if (config.iters == 0) record(evaluate(false));
+    // the iteration (fit3d.cpp:104-184) runs inside the library: this rank's views, the gradient
+    // all-reduce over the ranks (none with one rank), the Adam step
+    std::vector<double> local_cameras;
+    std::vector<const float*> local_targets;
+    for (std::size_t v = (std::size_t)shard.rank; v < views.size(); v += (std::size_t)shard.world) {
+        local_cameras.insert(local_cameras.end(), blocks[v].begin(), blocks[v].end());
+        local_targets.push_back(d_targets[v].data());
+    }
     for (int it = 1; it <= config.iters; ++it) {
-        record(evaluate(true));
-        throw_status(darbs_cuda_adam_step(ctx, (int64_t)dim, d_params.data(), d_grads.data(), d_m.data(), d_v.data(),
-                                          d_lrs.data(), it, DARBS_DEVICE),
+        double mean[4];
+        throw_status(darbs_cuda_train_step(ctx, &ks, psi, (int64_t)n, d_params.data(), d_grads.data(), d_m.data(),
+                                           d_v.data(), d_lrs.data(), (int)local_targets.size(), local_cameras.data(),
+                                           local_targets.data(), config.lambda, bg, it, (int)views.size(), mean),
                      ctx);
+        IterStats s;
+        s.loss = mean[0];
+        s.l1 = mean[1];
+        s.dssim = mean[2];
+        s.mse = mean[3];
+        record(s);
     }
 
     params = d_params.download();

@@ -58,3 +58,56 @@ def test_trainer_matches_the_serial_view_loop(port, darbs):
     # gradient is well away from zero
     big = np.abs(g_ref).reshape(-1) > 1e-6
     assert np.abs(params.reshape(-1) - p_ref)[big].max() <= 1e-5
+
+
+def test_train_step_matches_the_view_loop_with_a_one_rank_communicator(darbs):
+    """darbs_cuda_train_step (the C ABI's fit_scene iteration: local views, NCCL all-reduce in pieces
+    on a side stream, Adam piece by piece) against the same iteration spelled out with
+    evaluate_view + adam_step.  A world-size-1 NCCL communicator makes the all-reduce the identity,
+    so the NCCL call site, its stream hand-off and the piecewise Adam all run on one GPU; in the
+    deterministic mode the two spellings must agree bit for bit."""
+    import torch
+
+    from paper_2501_12369_b200 import synthetic as syn
+
+    name, n, n_views, w, h = "gaussian", 3000, 3, 96, 64
+    gk, psi = darbs.kernel_preset(name), darbs.default_psi(name)
+    truth = syn.scene_b(n, 1, half_extent=(0.5, 0.4, 0.4), scale_range=(0.01, 0.04))
+    init = syn.perturb(truth, 2)
+    cams = [syn.orbit_camera(v, n_views, w, h, 90.0) for v in range(n_views)]
+    dev = torch.device("cuda", 0)
+    lrs = torch.from_numpy(syn.learning_rates(init).reshape(-1)).to(dev)
+    results = []
+    for use_train_step in (False, True):
+        with darbs.Context(0) as ctx:
+            ctx.use_torch_stream()
+            ctx.set_deterministic(True)
+            truth_d = torch.from_numpy(truth).to(dev)
+            targets = []
+            for cam in cams:
+                t = torch.empty((h, w, 3), dtype=torch.float32, device=dev)
+                ctx.evaluate_view(gk, psi, truth_d, cam, (0, 0, 0), grad_image=torch.zeros_like(t), image_out=t)
+                targets.append(t)
+            p = torch.from_numpy(init).to(dev).clone()
+            g = torch.zeros_like(p)
+            m, v = torch.zeros(14 * n, device=dev), torch.zeros(14 * n, device=dev)
+            losses = []
+            if use_train_step:
+                ctx.comm_init(darbs.comm_unique_id(), 0, 1)
+            for it in (1, 2, 3):
+                if use_train_step:
+                    losses.append(ctx.train_step(gk, psi, p, g, m, v, lrs, cams, targets, 0.2, it, n_views))
+                else:
+                    sums = np.zeros(4)
+                    for i, cam in enumerate(cams):
+                        sums += ctx.evaluate_view(gk, psi, p, cam, (0, 0, 0), target=targets[i], lam=0.2, param_grads=g,
+                                                  accumulate=i > 0)
+                    ctx.adam_step(p.view(-1), g.view(-1), m, v, lrs, it)
+                    losses.append(tuple(sums / n_views))
+            torch.cuda.synchronize()
+            results.append((p.cpu().numpy(), g.cpu().numpy(), np.array(losses)))
+    (p0, g0, l0), (p1, g1, l1) = results
+    assert np.array_equal(g0, g1)
+    assert np.array_equal(p0, p1)
+    assert np.abs(l0 - l1).max() <= 1e-12 * np.abs(l0).max()
+    assert np.abs(p0 - init).max() > 1e-5 and l0[2, 0] < l0[0, 0]  # it did train
