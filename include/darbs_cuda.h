@@ -309,6 +309,13 @@ DARBS_API darbs_status darbs_cuda_comm_unique_id(darbs_comm_id* out);
 DARBS_API darbs_status darbs_cuda_comm_init(darbs_cuda_ctx* ctx, const darbs_comm_id* id, int rank,
                                             int world);
 DARBS_API darbs_status darbs_cuda_comm_destroy(darbs_cuda_ctx* ctx);
+/* The exchange and the update alone (fit3d.cpp:148-158's "+=" across ranks, then optim.hpp:24-39):
+ * grads[dim] (DARBS_DEVICE, already holding this rank's views) is all-reduced over the context's
+ * communicator in pieces on a side stream and Adam step t follows piece by piece.  For callers
+ * that evaluate their views themselves (e.g. with host-resident target images). */
+DARBS_API darbs_status darbs_cuda_allreduce_adam_step(darbs_cuda_ctx* ctx, int64_t dim, float* params,
+                                                      float* grads, float* m, float* v,
+                                                      const float* lrs, int t);
 /* One iteration.  All arrays are DARBS_DEVICE: params, grads, m, v, lrs [14 n]; cameras
  * [n_local_views][22]; targets[n_local_views] device pointers to [3wh] images of the cameras'
  * sizes.  The rank's local views are evaluated (the first overwrites `grads`, fit3d.cpp:107),

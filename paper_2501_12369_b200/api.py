@@ -111,6 +111,7 @@ def _load():
     lib.darbs_cuda_comm_unique_id.argtypes = [C.c_char_p]
     lib.darbs_cuda_comm_init.argtypes = [vp, C.c_char_p, i32, i32]
     lib.darbs_cuda_comm_destroy.argtypes = [vp]
+    lib.darbs_cuda_allreduce_adam_step.argtypes = [vp, i64, vp, vp, vp, vp, vp, i32]
     lib.darbs_cuda_train_step.argtypes = [vp, C.POINTER(KernelSpec), dbl, i64, vp, vp, vp, vp, vp, i32, C.POINTER(dbl),
                                           C.POINTER(vp), dbl, C.POINTER(C.c_float), i32, i32, C.POINTER(dbl)]
     lib.darbs_cuda_set_stage_timing.argtypes = [vp, i32]
@@ -129,7 +130,8 @@ EXPORTED_SYMBOLS = (
     "darbs_cuda_evaluate_view darbs_cuda_prefetch_target darbs_cuda_pop_loss darbs_cuda_adam_step darbs_cuda_set_stage_timing darbs_cuda_stage_times "
     "darbs_cuda_work_counters darbs_cuda_microbench darbs_cuda_loss_total darbs_cuda_device_alloc "
     "darbs_cuda_device_free darbs_cuda_upload darbs_cuda_download darbs_cuda_device_zero darbs_cuda_set_accumulate "
-    "darbs_cuda_comm_unique_id darbs_cuda_comm_init darbs_cuda_comm_destroy darbs_cuda_train_step"
+    "darbs_cuda_comm_unique_id darbs_cuda_comm_init darbs_cuda_comm_destroy darbs_cuda_train_step "
+    "darbs_cuda_allreduce_adam_step"
 ).split()
 
 
@@ -495,6 +497,12 @@ class Context:
 
     def comm_destroy(self):
         self._check(_lib.darbs_cuda_comm_destroy(self._h))
+
+    def allreduce_adam_step(self, params, grads, m, v, lrs, t: int):
+        """All-reduce of the gradients over the communicator (if any), then Adam step t; CUDA tensors."""
+        ptr = lambda a: C.c_void_p(a.data_ptr())  # noqa: E731
+        self._check(_lib.darbs_cuda_allreduce_adam_step(self._h, params.numel(), ptr(params), ptr(grads), ptr(m), ptr(v),
+                                                        ptr(lrs), t))
 
     def train_step(self, kernel: KernelSpec, psi: float, params, grads, m, v, lrs, cameras, targets, lam: float,
                    t: int, n_views_total: int, background=(0.0, 0.0, 0.0), want_loss: bool = True):

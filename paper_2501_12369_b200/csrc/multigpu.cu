@@ -156,6 +156,46 @@ darbs_status darbs_cuda_comm_destroy(darbs_cuda_ctx* ctx) {
     return DARBS_OK;
 }
 
+darbs_status darbs_cuda_allreduce_adam_step(darbs_cuda_ctx* ctx, int64_t dim_, float* params, float* grads, float* m,
+                                            float* v, const float* lrs, int t) {
+    if (!ctx) return fail(nullptr, DARBS_INVALID_PARAMETER, "context is NULL");
+    if (dim_ < 0 || t < 1) return fail(ctx, DARBS_INVALID_PARAMETER, "allreduce_adam_step: bad dim or step");
+    if (dim_ > 0 && (!params || !grads || !m || !v || !lrs))
+        return fail(ctx, DARBS_INVALID_PARAMETER, "allreduce_adam_step: NULL array");
+    Comm* c = (Comm*)ctx->comm;
+    const int world = c ? c->world : 1;
+    const size_t dim = (size_t)dim_;
+    int prev = -1;
+    cudaGetDevice(&prev);
+    if (prev != ctx->device) cudaSetDevice(ctx->device);
+    struct Restore {
+        int prev, dev;
+        ~Restore() {
+            if (prev >= 0 && prev != dev) cudaSetDevice(prev);
+        }
+    } restore{prev, ctx->device};
+    std::string why;
+    NcclApi* api = world > 1 ? nccl_api(&why) : nullptr;
+    if (world > 1 && !api) return fail(ctx, DARBS_CUDA_ERROR, "NCCL is not available: " + why);
+    if (world > 1) {
+        DARBS_CUDA_TRY(ctx, cudaEventRecord(c->grads_ready, ctx->stream));
+        DARBS_CUDA_TRY(ctx, cudaStreamWaitEvent(c->stream, c->grads_ready, 0));
+    }
+    const size_t piece = ((dim + kChunks - 1) / kChunks + 3) & ~(size_t)3;
+    for (int i = 0; i < kChunks; ++i) {
+        const size_t lo = (size_t)i * piece, hi = lo + piece < dim ? lo + piece : dim;
+        if (lo >= hi) break;
+        if (world > 1) {
+            const int rc = api->AllReduce(grads + lo, grads + lo, hi - lo, kNcclFloat32, kNcclSum, c->comm, c->stream);
+            if (rc != 0) return nccl_fail(ctx, api, rc, "ncclAllReduce");
+            DARBS_CUDA_TRY(ctx, cudaEventRecord(c->piece_done[i], c->stream));
+            DARBS_CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->stream, c->piece_done[i], 0));
+        }
+        DARBS_TRY(launch_adam(ctx, (int64_t)(hi - lo), params + lo, grads + lo, m + lo, v + lo, lrs + lo, t));
+    }
+    return DARBS_OK;
+}
+
 darbs_status darbs_cuda_train_step(darbs_cuda_ctx* ctx, const darbs_kernel_spec* kernel, double psi, int64_t n,
                                    float* params, float* grads, float* m, float* v, const float* lrs,
                                    int n_local_views, const double* cameras, const float* const* targets,
@@ -207,25 +247,14 @@ darbs_status darbs_cuda_train_step(darbs_cuda_ctx* ctx, const darbs_kernel_spec*
     }
 
     // gradients summed over all ranks' views, in kChunks pieces; Adam follows piece by piece
-    std::string why;
-    NcclApi* api = world > 1 ? nccl_api(&why) : nullptr;
-    if (world > 1 && !api) return fail(ctx, DARBS_CUDA_ERROR, "NCCL is not available: " + why);
-    if (world > 1) {
-        DARBS_CUDA_TRY(ctx, cudaEventRecord(c->grads_ready, ctx->stream));
-        DARBS_CUDA_TRY(ctx, cudaStreamWaitEvent(c->stream, c->grads_ready, 0));
-    }
-    const size_t piece = ((dim + kChunks - 1) / kChunks + 3) & ~(size_t)3;
-    for (int i = 0; i < kChunks; ++i) {
-        const size_t lo = (size_t)i * piece, hi = lo + piece < dim ? lo + piece : dim;
-        if (lo >= hi) break;
-        if (world > 1) {
-            const int rc = api->AllReduce(grads + lo, grads + lo, hi - lo, kNcclFloat32, kNcclSum, c->comm, c->stream);
-            if (rc != 0) return nccl_fail(ctx, api, rc, "ncclAllReduce");
-            DARBS_CUDA_TRY(ctx, cudaEventRecord(c->piece_done[i], c->stream));
-            DARBS_CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->stream, c->piece_done[i], 0));
+    {
+        const darbs_status st = darbs_cuda_allreduce_adam_step(ctx, (int64_t)dim, params, grads, m, v, lrs, t);
+        if (st != DARBS_OK) {
+            while (pending > 0) collect();
+            return st;
         }
-        DARBS_TRY(launch_adam(ctx, (int64_t)(hi - lo), params + lo, grads + lo, m + lo, v + lo, lrs + lo, t));
     }
+    NcclApi* api = world > 1 ? nccl_api(nullptr) : nullptr;
     while (pending > 0) collect();
     if (view_status != DARBS_OK) return view_status;
 

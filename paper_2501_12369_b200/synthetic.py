@@ -78,3 +78,22 @@ def sample_workload(n_full: int, width: int, height: int, focal: float, fraction
     assert s * s == fraction
     return dict(n=n_full // fraction, width=width // s, height=height // s, focal=focal,
                 half_extent=(1.8 / s, 1.0 / s, 1.0))
+
+
+def scene_a(n: int, width: int, height: int, seed: int, cutoff: float = 9.0):
+    """The reference's 2-D `random_scene` distribution (benchmarks/bench.cpp:20-46, SURVEY.md 8d
+    "input A") with numpy's generator: covariance entries a, c ~ U[0.6, 12] px^2,
+    b = U[-0.6, 0.6] sqrt(ac), centres up to 5 px outside the image, depth ~ U[0.5, 9.5], opacity ~
+    U[0.1, 0.95], colour ~ U[0, 1]^3; conic and radius as conic_and_radius (geometry.cpp:50-64) gives
+    them for a kernel with the given cutoff.  Returns float32 arrays in the forward ABI's layout."""
+    rng = np.random.default_rng(seed)
+    a = rng.uniform(0.6, 12.0, n)
+    c = rng.uniform(0.6, 12.0, n)
+    b = rng.uniform(-0.6, 0.6, n) * np.sqrt(a * c)
+    det = a * c - b * b
+    lam1 = 0.5 * (a + c) + np.sqrt(np.maximum(0.25 * (a - c) ** 2 + b * b, 0.0))
+    f32 = lambda x: np.ascontiguousarray(x, dtype=np.float32)  # noqa: E731
+    return dict(mu2=f32(np.stack([rng.uniform(-5.0, width + 5.0, n), rng.uniform(-5.0, height + 5.0, n)], axis=1)),
+                conic=f32(np.stack([c / det, -b / det, a / det], axis=1)),
+                radius=f32(np.ceil(np.sqrt(cutoff) * np.sqrt(lam1))), depth=f32(rng.uniform(0.5, 9.5, n)),
+                opacity=f32(rng.uniform(0.1, 0.95, n)), rgb=f32(rng.uniform(0.0, 1.0, (n, 3))))
