@@ -346,7 +346,10 @@ darbs_status darbs_cuda_create(int device, darbs_cuda_ctx** out_ctx) {
     ctx->timer.created = true;
     cudaEventCreateWithFlags(&ctx->after_cull, cudaEventDisableTiming);
     cudaEventCreateWithFlags(&ctx->k_ready, cudaEventDisableTiming);
-    for (int i = 0; i < 2; ++i) cudaEventCreateWithFlags(&ctx->target_done[i], cudaEventDisableTiming);
+    for (int i = 0; i < 2; ++i) {
+        cudaEventCreateWithFlags(&ctx->target_done[i], cudaEventDisableTiming);
+        cudaEventCreateWithFlags(&ctx->target_read[i], cudaEventDisableTiming);
+    }
     for (int i = 0; i < kLossRing; ++i) {
         cudaMallocHost(&ctx->loss_ring[i].host, 64);
         cudaEventCreateWithFlags(&ctx->loss_ring[i].done, cudaEventDisableTiming);
@@ -390,6 +393,7 @@ void darbs_cuda_destroy(darbs_cuda_ctx* ctx) {
     if (ctx->k_ready) cudaEventDestroy(ctx->k_ready);
     for (int i = 0; i < 2; ++i) {
         if (ctx->target_done[i]) cudaEventDestroy(ctx->target_done[i]);
+        if (ctx->target_read[i]) cudaEventDestroy(ctx->target_read[i]);
         if (ctx->target_stage[i].ptr) cudaFree(ctx->target_stage[i].ptr);
     }
     if (ctx->copy_begin) cudaEventDestroy(ctx->copy_begin);
@@ -847,6 +851,10 @@ darbs_status darbs_cuda_evaluate_view(darbs_cuda_ctx* ctx, const darbs_kernel_sp
         }
         DARBS_TRY(launch_loss(ctx, width, height, d_image, d_target, lambda, d_lgrad, d_sums));
         d_gimg = d_lgrad;
+        if (staged >= 0) {  // the slot's last reader: a later prefetch into it waits for this
+            DARBS_CUDA_TRY(ctx, cudaEventRecord(ctx->target_read[staged], ctx->stream));
+            ctx->target_read_pending[staged] = true;
+        }
     }
     if (param_grads) {
         {
@@ -912,6 +920,10 @@ darbs_status darbs_cuda_prefetch_target(darbs_cuda_ctx* ctx, const float* host_i
     } else {
         DARBS_CUDA_TRY(ctx, cudaEventRecord(ctx->copy_begin, ctx->stream));
         DARBS_CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->copy_stream, ctx->copy_begin, 0));
+    }
+    if (ctx->target_read_pending[slot]) {  // the loss kernels that read the slot's previous image
+        DARBS_CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->copy_stream, ctx->target_read[slot], 0));
+        ctx->target_read_pending[slot] = false;
     }
     DARBS_CUDA_TRY(ctx, cudaMemcpyAsync(ctx->target_stage[slot].ptr, host_image, sizeof(float) * (size_t)count,
                                         cudaMemcpyHostToDevice, ctx->copy_stream));

@@ -178,22 +178,41 @@ expand_kernel(unsigned n, const unsigned* __restrict__ order, const uint2* __res
             }
         }
     }
-    // entries of all earlier CTAs: decoupled look-back, 32 predecessors per round trip
+    // entries of all earlier CTAs: decoupled look-back, 128 predecessors per round trip (every CTA
+    // of a million-splat view is resident at once, so the walk is rounds of L2 latency, not waiting)
     if (warp == 0) {
         unsigned excl = 0;
         long long c = (long long)chunk - 1;
         while (c >= 0) {
-            const long long at = c - lane;
-            const unsigned s = at >= 0 ? radix::ld_relaxed(status + at) : radix::kInclusive;
-            if (!__all_sync(full, (s >> 30) != 0u)) continue;  // someone has not published yet
-            const unsigned incl = __ballot_sync(full, (s >> 30) == 2u);
-            const int stop = incl ? __ffs(incl) - 1 : 31;
-            unsigned v = lane <= stop ? (s & radix::kValue) : 0u;
+            constexpr int kRounds = 4;
+            unsigned s[kRounds];
 #pragma unroll
-            for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(full, v, o);
-            excl += v;
-            if (incl) break;
-            c -= 32;
+            for (int r = 0; r < kRounds; ++r) {
+                const long long at = c - 32 * r - lane;
+                s[r] = at >= 0 ? radix::ld_relaxed(status + at) : radix::kInclusive;
+            }
+            bool done = false;
+            int used = 0;
+#pragma unroll
+            for (int r = 0; r < kRounds; ++r) {
+                if (done) continue;
+                if (!__all_sync(full, (s[r] >> 30) != 0u)) {  // someone has not published yet: poll again from here
+                    done = true;
+                    continue;
+                }
+                const unsigned incl = __ballot_sync(full, (s[r] >> 30) == 2u);
+                const int stop = incl ? __ffs(incl) - 1 : 31;
+                unsigned v = lane <= stop ? (s[r] & radix::kValue) : 0u;
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(full, v, o);
+                excl += v;
+                used = r + 1;
+                if (incl) {
+                    done = true;
+                    c = -1 - 32 * used;  // leaves the walk
+                }
+            }
+            c -= 32 * used;
         }
         if (lane == 0) {
             if (chunk > 0) radix::st_relaxed(status + chunk, (excl + cta_total) | radix::kInclusive);

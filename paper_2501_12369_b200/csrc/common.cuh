@@ -40,9 +40,9 @@ struct KParams {
 
 // Packed per-splat record, 4 x float4 = 64 B, 64-B aligned (two 32-B sectors
 // per gather for the three hot vectors):
-//   v0 = { mu.x, mu.y, A = scale*a, B = scale*2b }
-//   v1 = { C = scale*c, opacity, thr_m, -b/c }  thr_m: see family_threshold()
-//   v2 = { r, g, b, -b/a }                       v1.w, v2.w: block-cull helpers
+//   v0 = { mu.x, mu.y, A = scale*a, C = scale*c }   (A, C) adjacent: one packed multiply with (dx^2, dy^2)
+//   v1 = { B = scale*2b, opacity, thr_m, -b/c }     thr_m: see family_threshold()
+//   v2 = { r, g, b, -b/a }                          v1.w, v2.w: block-cull helpers
 //   v3 = { a, b, c, 0 }                          unscaled conic for the FP64 path
 static constexpr int kRecVecs = 4;
 
@@ -123,6 +123,8 @@ struct darbs_cuda_ctx {
     darbs_b200::DeviceBuffer target_stage[2];
     const void* target_src[2] = {nullptr, nullptr};
     cudaEvent_t target_done[2] = {nullptr, nullptr};
+    cudaEvent_t target_read[2] = {nullptr, nullptr};  // recorded behind the slot's last reader (the loss kernels)
+    bool target_read_pending[2] = {false, false};
     int target_next = 0;
     cudaEvent_t after_cull = nullptr;  // the last forward's long kernels start here
     cudaEvent_t k_ready = nullptr;     // binning: the entry count K has reached pinned host memory

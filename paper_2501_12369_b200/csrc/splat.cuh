@@ -55,6 +55,8 @@ __device__ __forceinline__ void accumulate_tile_count(unsigned cnt, unsigned lon
         atomicAdd(k_slots + (blockIdx.x & (kSlotsK - 1)), (unsigned long long)sum);
 }
 
+constexpr double kMaxKappa = 50.0;  // largest eigenvalue ratio of a conic the float32 decisions are trusted with
+
 __device__ __forceinline__ void splat_record(const KParams& kp, float mx, float my, float a, float b, float c,
                                              float o, float cr, float cg, float cb, float4* __restrict__ r) {
     double ad = a, bd = b, cd = c;
@@ -62,6 +64,14 @@ __device__ __forceinline__ void splat_record(const KParams& kp, float mx, float 
     // An indefinite or non-finite conic cannot be culled by the convex block
     // test and may produce dm2 < 0 (rasterizer.cpp:91): force the FP64 path.
     bool pd = (ad > 0.0) && (cd > 0.0) && (ad * cd - bd * bd > 0.0);
+    // The float32 quadratic form A dx^2 + B dx dy + C dy^2 is evaluated in absolute pixel offsets:
+    // its terms reach kappa * m (kappa = the conic's eigenvalue ratio) and cancel down to m, so its
+    // error is ~3 eps kappa m.  Past kappa = kMaxKappa that leaves the guard band (1e-4 at m ~ 10):
+    // such needles (sigma 100 px against the 0.3 px^2 dilation floor) take every decision in FP64.
+    if (pd) {
+        const double tr = ad + cd, disc = sqrt((ad - cd) * (ad - cd) + 4.0 * bd * bd);
+        pd = (tr + disc) <= kMaxKappa * (tr - disc);
+    }
     float thr_m = pd ? (float)(thr * (double)kp.scale) : __int_as_float(0x7fc00000);
     // (A, C) adjacent: they meet (dx, dy) in one packed multiply (quad_m, render.cu)
     r[0] = make_float4(mx, my, kp.scale * a, kp.scale * c);

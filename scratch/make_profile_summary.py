@@ -26,7 +26,46 @@ KEYS = [
     ("dram__throughput.avg.pct_of_peak_sustained_elapsed", "DRAM throughput %"),
     ("lts__t_sector_hit_rate.pct", "L2 hit rate %"), ("l1tex__t_sector_hit_rate.pct", "L1 hit rate %"),
     ("lts__t_sectors_op_red.sum", "L2 sectors, reductions (red.global)"),
+    ("lts__t_sectors_op_atom.sum", "L2 sectors, atomics with return (atom.global)"),
+    ("smsp__inst_executed_op_global_red.sum", "warp instructions, red.global"),
+    ("smsp__inst_executed_op_global_atom.sum", "warp instructions, atom.global"),
+    ("smsp__inst_executed_op_shared_atom.sum", "warp instructions, shared-memory atomics"),
+    ("l1tex__t_set_accesses_pipe_lsu_mem_global_op_red.sum", "L1 set accesses, red.global"),
 ]
+
+
+def derived(d, units, hdr):
+    """achieved DRAM GB/s and reduction / atomic throughput: counter / kernel duration"""
+    def num(k):
+        try:
+            return float(d[k].replace(",", ""))
+        except (KeyError, ValueError):
+            return None
+
+    def in_unit(k, scale):
+        v = num(k)
+        if v is None:
+            return None
+        u = units[hdr.index(k)]
+        return v * scale.get(u, 1.0)
+
+    dur = in_unit("gpu__time_duration.sum", {"us": 1e-6, "usecond": 1e-6, "ms": 1e-3, "msecond": 1e-3, "ns": 1e-9, "nsecond": 1e-9, "s": 1.0, "second": 1.0})
+    if not dur:
+        return []
+    byt = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+    rd, wr = in_unit("dram__bytes_read.sum", byt), in_unit("dram__bytes_write.sum", byt)
+    out = []
+    if rd is not None and wr is not None:
+        out.append(f"| **achieved HBM traffic** | {(rd + wr) / dur / 1e9:,.0f} GB/s ({(rd + wr) / 1e6:,.1f} MB in {dur * 1e6:,.1f} us) |")
+    red, atom = num("lts__t_sectors_op_red.sum"), num("lts__t_sectors_op_atom.sum")
+    if red is not None and (red or atom):
+        out.append(f"| **atomic throughput at L2** | {red / dur / 1e9:,.2f} G red-sectors/s"
+                   + (f", {atom / dur / 1e9:,.2f} G atom-sectors/s" if atom else "") + " |")
+    ri = num("smsp__inst_executed_op_global_red.sum")
+    if ri:
+        out.append(f"| red.global warp instructions per second | {ri / dur / 1e9:,.3f} G/s |")
+    return out
+
 raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(raw)))
 hdr, units = rows[0], rows[1]
@@ -48,6 +87,7 @@ for r in rows[2:]:
             except ValueError:
                 pass
             lines.append(f"| {label} | {v} {units[hdr.index(k)]} |")
+    lines += derived(d, units, hdr)
     lines.append("")
 src = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv"], capture_output=True, text=True).stdout
 done = set()

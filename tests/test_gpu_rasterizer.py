@@ -196,6 +196,42 @@ def test_forward_parity_opaque(ctx, port, name):
     run_forward_parity(ctx, port, name, 2500, 90, 70, 13, opaque=True)
 
 
+@pytest.mark.parametrize("name", ["gaussian", "half-cosine-sq", "raised-cosine"])
+def test_forward_and_backward_parity_needle_splats(ctx, port, name):
+    """Ill-conditioned conics: sigma ~ 100 px along one axis against the 0.3 px^2 dilation
+    floor along the other, at every angle.  In absolute pixel offsets the float32 quadratic form
+    of such a needle carries an error far beyond the guard band, so the library takes their
+    decisions in FP64 (splat.cuh kMaxKappa): processed / contributors stay the oracle's."""
+    k = oracle_kernel(port, name)
+    n, w, h = 400, 160, 128
+    s = port.random_scene(k, n, w, h, 3)
+    rng = np.random.default_rng(5)
+    ang = rng.uniform(0, np.pi, n)
+    s1 = rng.uniform(40.0, 120.0, n) ** 2
+    s2 = np.full(n, 0.3) + rng.uniform(0.0, 0.5, n)
+    needle = rng.uniform(size=n) < 0.5  # the other half stays well conditioned: both paths share streams
+    c, sn = np.cos(ang), np.sin(ang)
+    cov = np.stack([c * c * s1 + sn * sn * s2, c * sn * (s1 - s2), sn * sn * s1 + c * c * s2], axis=1)  # xx, xy, yy
+    st, conic, radius, _lam = port.conic_and_radius(k, cov[needle])
+    assert st == 0
+    s.conic[needle] = f32(conic).astype(np.float64)  # float32-representable, as every parity input
+    s.radius[needle] = radius
+    s.opacity[needle] = f32(rng.uniform(0.05, 0.4, int(needle.sum())))
+    g = port.random_image_grad(w, h, 9)
+    fr = port.forward(k, s, w, h, BG, threads=0, keep=True)
+    st, ref_g = port.backward(fr["handle"], k, g, s, threads=0)
+    port.forward_free(fr["handle"])
+    out = ctx.forward(gpu_kernel_cached(name), **scene_f32(s), width=w, height=h, background=BG)
+    assert np.array_equal(out["processed"], fr["processed"])
+    assert np.array_equal(out["contributors"], fr["contributors"])
+    assert np.abs(out["image"] - fr["image"]).max() <= IMG_TOL
+    got = ctx.backward(gpu_kernel_cached(name), f32(g), n)
+    # decisions are exact, but the weight and its derivative still see the float32 quadratic form, whose
+    # relative error grows with the eigenvalue ratio (~3 eps kappa, kappa up to 5e4 here): 5e-3 instead
+    # of 1e-3 (measured: 1.4e-3 for the raised cosine, whose dw/dm ~ 1/sqrt(m); < 1e-3 for the others)
+    assert grad_err(got, ref_g).max() <= 5.0 * GRAD_TOL
+
+
 def test_transmittance_floor_pixels_are_exact(ctx, port):
     """The last decision of a pixel, T < 1e-4 (rasterizer.cpp:100), cannot be taken in FP32 when T
     ends within a few 1e-9 of the floor: the forward kernel composites those pixels again in FP64
