@@ -60,6 +60,9 @@ def parse_args():
     ap.add_argument("--height", type=int, default=1080)
     ap.add_argument("--focal", type=float, default=1600.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--table", action="store_true",
+                    help="with --impl reference: time the reference's CPU code on BASELINE.json configs[0] and "
+                         "configs[1] too (the rows of BASELINE.md section 4) instead of the headline workload")
     ap.add_argument("--exact", type=int, default=1, help="FP64 guard-band re-decisions (default on)")
     args = ap.parse_args()
     if args.config is None:
@@ -182,6 +185,56 @@ def cpu_target(orc, cpu, name, truth, cam, threads):
     s = cpu.Scene(pr["mu2"][vis], None, pr["conic"][vis], pr["radius"][vis], pr["depth"][vis], prims[vis, 10],
                   prims[vis, 11:14])
     return orc.forward(k, s, int(cam[4]), int(cam[5]), (0.0, 0.0, 0.0), threads=threads)["image"]
+
+
+def reference_table(args):
+    """The CPU side of BASELINE.md section 4 for the configurations bench.py's headline does not cover:
+    configs[0] (10 k random splats, 256 x 256, half-cosine-sq, forward + backward; input A, the reference's
+    own random_scene) and configs[1] (1 M splats 1080p forward render per kernel; scene B projected by the
+    reference's own project_primitive).  The reference's own sources (oracle/_ref), steady clock around the
+    calls, 1 warm-up + 3 repetitions (1 at 1 M splats)."""
+    from oracle import cpu
+    from paper_2501_12369_b200 import synthetic as syn
+
+    kind = "reference" if cpu.available("reference") else "port"
+    orc = cpu.load(kind)
+    threads = os.cpu_count() or 1
+    out = {"impl": "reference", "kind": kind, "cores": threads}
+    k = orc.preset("half-cosine-sq")
+    s = orc.random_scene(k, 10_000, 256, 256, 0)
+    g = orc.random_image_grad(256, 256, 32)
+    rows = {}
+    for th in (threads, 1):
+        tf = tb = 0.0
+        for rep in range(4):
+            t0 = time.perf_counter()
+            fr = orc.forward(k, s, 256, 256, (0.1, 0.2, 0.3), threads=th, keep=True)
+            t1 = time.perf_counter()
+            orc.backward(fr["handle"], k, g, s, threads=th)
+            t2 = time.perf_counter()
+            orc.forward_free(fr["handle"])
+            if rep:
+                tf += (t1 - t0) / 3
+                tb += (t2 - t1) / 3
+        rows[f"{th}_threads"] = {"ms_forward": 1e3 * tf, "ms_backward": 1e3 * tb}
+    out["config0_10k_256_half-cosine-sq"] = rows
+    truth = syn.scene_b(args.splats, 1)
+    cam = syn.orbit_camera(0, 1, args.width, args.height, args.focal)
+    fwd = {}
+    for name in ("gaussian", "half-cosine-sq", "raised-cosine"):
+        kk, psi = orc.preset(name), orc.default_psi(name)
+        t0 = time.perf_counter()
+        prims = orc.realize(truth.astype(np.float64))
+        st, pr = orc.project(kk, psi, prims, cam)
+        vis = np.flatnonzero(pr["valid"])
+        sc = cpu.Scene(pr["mu2"][vis], None, pr["conic"][vis], pr["radius"][vis], pr["depth"][vis], prims[vis, 10],
+                       prims[vis, 11:14])
+        t1 = time.perf_counter()
+        orc.forward(kk, sc, args.width, args.height, (0.0, 0.0, 0.0), threads=threads)
+        t2 = time.perf_counter()
+        fwd[name] = {"ms_preprocess": 1e3 * (t1 - t0), "ms_forward_incl_bin": 1e3 * (t2 - t1), "fps": 1.0 / (t2 - t0)}
+    out[f"config1_{args.splats}_splats_{args.width}x{args.height}_forward"] = fwd
+    print(json.dumps(out), flush=True)
 
 
 def run_reference_arm(args):
@@ -838,7 +891,10 @@ def cpu_baseline(args, single_thread=True):
 
 def main():
     args = parse_args()
-    if args.impl == "reference":
+    if args.impl == "reference" and args.table:
+        args.splats = args.splats or 1_000_000
+        reference_table(args)
+    elif args.impl == "reference":
         run_reference_arm(args)
     elif args.config == 3:
         run_config3(args)

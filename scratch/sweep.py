@@ -43,7 +43,8 @@ def run(name, n, w, h, focal, reps=5):
     return dict(zip(STAGES, med)), wc
 
 
-lines = ["# Round 1 - kernel sweep at 3840x2160 and forward FPS at 1080p (B200, device-resident, CUDA events)", "",
+lines = ["# Round 2 - DARBF kernel sweep at 3840x2160, forward render FPS at 1080p, and the 10 k-splat case (one B200)", "",
+         "`scratch/sweep.py`: device-resident, CUDA-event stage times, median of 5 after 2 warm-ups; BASELINE.json `configs[4]`, `configs[1]`, `configs[0]`.", "",
          "Scene B of bench.py scaled to the resolution (focal 3200 at 4K), one orbit view, full training iteration "
          "(preprocess, bin+sort, cull, render fwd, L1 + D-SSIM loss, render bwd, preprocess bwd, Adam); "
          "stage times in ms, median of 5.", "",
@@ -65,4 +66,20 @@ for name in KERNELS + ["mod-sinc"]:
     ms = t["preprocess"] + t["binning"] + t["cull"] + t["render_fwd"]
     lines.append(f"| {name} | {t['preprocess']:.3f} | {t['binning']:.3f} | {t['cull']:.3f} | {t['render_fwd']:.3f} | {ms:.3f} | {1e3 / ms:.0f} |")
     print(lines[-1], flush=True)
+# configs[0]: 10 k random splats (input A), 256 x 256, half-cosine-sq, forward + backward through the host-pointer ABI
+import time
+sc = syn.scene_a(10_000, 256, 256, 0)
+k = d.kernel_preset("half-cosine-sq")
+arrs = [sc[key] for key in ("mu2", "conic", "radius", "depth", "opacity", "rgb")]
+g = np.ones((256, 256, 3), np.float32)
+ctx.set_stage_timing(False)
+tf = tb = 0.0
+for rep in range(55):
+    t0 = time.perf_counter(); ctx.forward(k, *arrs, 256, 256, (0.1, 0.2, 0.3)); t1 = time.perf_counter()
+    ctx.backward(k, g, 10_000); t2 = time.perf_counter()
+    if rep >= 5:
+        tf += (t1 - t0) / 50; tb += (t2 - t1) / 50
+lines += ["", "## 10,000 random splats, 256x256, half-cosine-sq, forward + backward (BASELINE.json configs[0])", "",
+          f"Host arrays in and out through darbs_cuda_forward / darbs_cuda_backward (all copies inside the calls), mean of 50: "
+          f"forward {1e3 * tf:.3f} ms, backward {1e3 * tb:.3f} ms."]
 open(out, "w").write("\n".join(lines) + "\n")
