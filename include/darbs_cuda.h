@@ -118,6 +118,11 @@ DARBS_API darbs_status darbs_cuda_set_exact_decisions(darbs_cuda_ctx* ctx, int e
  * associative, so the result is bitwise independent of the order in which blocks arrive and a
  * rerun is bitwise identical.  0: float32 vector reductions (faster; equal up to summation order). */
 DARBS_API darbs_status darbs_cuda_set_deterministic(darbs_cuda_ctx* ctx, int enabled);
+/* Tuning knob without a reference analogue.  The cull kernel tests only the first `entries` list
+ * entries of every tile against its eight 8x4 pixel blocks; a block whose pixels are still live
+ * behind them culls on by itself inside the forward kernel.  Results do not depend on the value
+ * (the per-pixel walk is the reference's, rasterizer.cpp:85-107); 0 (default) picks per family. */
+DARBS_API darbs_status darbs_cuda_set_cull_segment(darbs_cuda_ctx* ctx, int entries);
 
 /* ---- device memory ----------------------------------------------------------
  * For callers without a CUDA toolchain of their own (the C++ mirror's fit_scene keeps the raw

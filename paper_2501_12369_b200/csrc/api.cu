@@ -893,6 +893,13 @@ darbs_status darbs_cuda_evaluate_view(darbs_cuda_ctx* ctx, const darbs_kernel_sp
     return DARBS_OK;
 }
 
+darbs_status darbs_cuda_set_cull_segment(darbs_cuda_ctx* ctx, int entries) {
+    CTX_OR_FAIL(ctx);
+    if (entries < 0) return fail(ctx, DARBS_INVALID_PARAMETER, "set_cull_segment: negative");
+    ctx->cull_segment = entries;
+    return DARBS_OK;
+}
+
 darbs_status darbs_cuda_set_deterministic(darbs_cuda_ctx* ctx, int enabled) {
     CTX_OR_FAIL(ctx);
     ctx->deterministic = enabled ? 1 : 0;

@@ -91,6 +91,7 @@ struct darbs_cuda_ctx {
     int64_t launches = 0;
     int exact = 1;
     int timing = 0;
+    int cull_segment = 0;   // entries of a tile's list the cull kernel covers (0: per family, render.cu cull_segment)
     int deterministic = 0;  // fixed-point accumulation of gradients and loss sums (darbs_cuda_set_deterministic)
     int accumulate = 1;  // evaluate_view adds to param_grads (0: the next call overwrites)
     double stage_ms[8] = {0, 0, 0, 0, 0, 0, 0, 0};

@@ -326,22 +326,25 @@ __device__ __forceinline__ bool block_survives(float A, float B, float C, float 
 // prefix over the eight warps give every survivor its slot, so streams keep list order.
 __global__ void __launch_bounds__(kThreads)
 cull_kernel(KParams kp, const float4* __restrict__ recs, const int2* __restrict__ ranges,
-            const int* __restrict__ point_list, int tiles_x, float4* __restrict__ streams,
+            const int* __restrict__ point_list, int tiles_x, int seg, float4* __restrict__ streams,
             int* __restrict__ stream_count, unsigned long long* __restrict__ counters) {
     __shared__ int wcnt[kWarpsPerCta][kBlocksPerTile];
     __shared__ int wpre[kWarpsPerCta][kBlocksPerTile];
     const int tile = blockIdx.x;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int2 range = ranges[tile];
-    const int beg = range.x, end = range.y;
+    const int beg = range.x, list_end = range.y;
+    // only the first `seg` entries of the list are culled here: the forward extends a block's stream
+    // itself when its pixels outlive them (extend_stream), and most blocks of a dense scene do not
+    const int end = list_end - beg > seg ? beg + seg : list_end;
     const float tx0 = (float)((tile % tiles_x) * DARBS_TILE_SIZE) + 0.5f;
     const float ty0 = (float)((tile / tiles_x) * DARBS_TILE_SIZE) + 0.5f;
     const float band2 = 2.f * kp.band;
     const unsigned lt_mask = (1u << lane) - 1u;
     // threads 0..63 keep the running stream length of block (tid & 7); the eight copies agree
     int run = 0;
-    float4* const tile_streams = streams + kEntryVecs * stream_offset(tile, beg, end, 0);
-    const size_t cap = (size_t)((end - beg + kChunk - 1) & ~(kChunk - 1));
+    float4* const tile_streams = streams + kEntryVecs * stream_offset(tile, beg, list_end, 0);
+    const size_t cap = (size_t)((list_end - beg + kChunk - 1) & ~(kChunk - 1));
 
     // software pipeline: list index two steps ahead, record one step ahead of the step under test
     int idx_n = beg + tid < end ? __ldg(point_list + beg + tid) : -1;
@@ -577,15 +580,103 @@ __device__ __forceinline__ void fwd_visit(const KParams& kp, const float4* __res
     px.T = fmaf(-alpha, px.T, px.T);
 }
 
+// The cull kernel covers only the first `seg` entries of a tile's list.  A block whose pixels are
+// still live at the end of its stream culls on by itself: the warp tests the next list entries
+// (lane = entry) against its own 8x4 block with the cull kernel's bound and appends the survivors
+// at position n of its stream, in list order, until a chunk's worth has been added or the list
+// ends; null padding follows up to a multiple of kPad, as behind every stream.  Returns the new
+// stream length.  Only this warp reads the new entries before the kernel ends (plain loads).
+__device__ __noinline__ int extend_stream(const KParams& kp, const float4* __restrict__ recs,
+                                          const int* __restrict__ list, int list_len, int& culled,
+                                          float4* __restrict__ dst, int n, float bx05, float by05, int lane) {
+    // (`culled` by reference: the callers are slow paths that hold it in a local of their own)
+    const float band2 = 2.f * kp.band;
+    const unsigned lt = (1u << lane) - 1u;
+    int count = 0;
+    while (culled < list_len && count < kChunk) {
+        const int k = culled + lane;
+        bool surv = false;
+        float4 v0 = make_float4(0.f, 0.f, 0.f, 0.f), v1 = v0, v2 = v0;
+        int idx = -1;
+        if (k < list_len) {
+            idx = __ldg(list + k);
+            const float4* r = recs + kRecVecs * (int64_t)idx;
+            v0 = __ldg(r);
+            v1 = __ldg(r + 1);
+            v2 = __ldg(r + 2);
+            const float ex0 = bx05 - v0.x, ex1 = ex0 + 7.f, dxc = fminf(fmaxf(0.f, ex0), ex1);
+            const float ey0 = by05 - v0.y, ey1 = ey0 + 3.f, dyc = fminf(fmaxf(0.f, ey0), ey1);
+            surv = block_survives(v0.z, v1.x, v0.w, v1.w, v2.w, v1.z + band2, dxc, ex0, ex1, dyc, ey0, ey1);
+        }
+        const unsigned m = __ballot_sync(kFull, surv);
+        if (surv) {
+            float4* e = dst + kEntryVecs * (size_t)(n + count + __popc(m & lt));
+            e[0] = v0;
+            e[1] = make_float4(v1.x, v1.y, v1.z, __int_as_float(k));
+            e[2] = make_float4(v2.x, v2.y, v2.z, __int_as_float(idx));
+        }
+        count += __popc(m);
+        culled = culled + 32 < list_len ? culled + 32 : list_len;
+    }
+    const int n_new = n + count;
+    const int padded = (n_new + kPad - 1) & ~(kPad - 1);
+    if (n_new + lane < padded) store_null_entry(dst + kEntryVecs * (size_t)(n_new + lane));
+    __threadfence();
+    __syncwarp();
+    return n_new;
+}
+
+// The slow path of the forward for a block that outlives the culled part of its list: composite
+// what the stream holds (whole groups; straight from global memory, no ring), extend the stream by
+// about a chunk, and so on until the pixels saturate or the list ends.  `pos` is the first stream
+// entry not yet composited; it comes back as the forward's `used`.  Always the clamp-aware visit.
+struct TailResult {  // by value in and out: nothing of the kernel's loop state has its address taken
+    FwdPixel px;
+    int pos, n, culled;
+};
+template <int FAM>
+__device__ __noinline__ TailResult forward_tail(const KParams& kp, const float4* __restrict__ recs,
+                                                const int* __restrict__ list, int list_len, int culled,
+                                                float4* __restrict__ dst, int n, int pos, float bx05, float by05,
+                                                float fx, float fy, int lane, FwdPixel px) {
+    constexpr int kGroup = FwdGroup<FAM>::value;
+    bool dead = false;
+    while (true) {
+        const bool last_round = culled >= list_len;
+        const int n_run = last_round ? n : n - n % kGroup;  // the last group may run into the null padding
+        for (; pos < n_run && !dead; pos += kGroup) {
+            const float4* qb = dst + (size_t)pos * kEntryVecs;
+            const FwdPixel save = px;
+            bool near_acc = false;
+            for (int j = 0; j < kGroup; ++j) fwd_visit<FAM, false, true>(kp, recs, qb + j * 3, fx, fy, px, near_acc);
+            if (kp.exact && __any_sync(kFull, near_acc)) {
+                px = save;
+                for (int j = 0; j < kGroup; ++j) fwd_visit<FAM, true, true>(kp, recs, qb + j * 3, fx, fy, px, near_acc);
+            }
+            dead = !__any_sync(kFull, !(px.T < kTFloorF));
+        }
+        if (dead || last_round) break;
+        n = extend_stream(kp, recs, list, list_len, culled, dst, n, bx05, by05, lane);
+    }
+    TailResult r;
+    r.px = px;
+    r.pos = pos;
+    r.n = n;
+    r.culled = culled;
+    return r;
+}
+
 // Warps of a forward CTA.  A warp owns one 8x4 block and leaves as soon as its 32 pixels have
 // saturated; with a whole tile (8 warps) per CTA the early leavers' slots idle until the CTA's
 // slowest warp is done, so CTAs are kept small and the hardware scheduler backfills.
 constexpr int kFwdWarps = 2;
 
-template <int FAM>
+// TAIL: the cull kernel covered only the first `seg` entries of the lists, so a block may have to
+// cull on by itself (forward_tail).  Without it the kernel is the plain stream walk.
+template <int FAM, bool TAIL>
 __global__ void __launch_bounds__(32 * kFwdWarps, 32 / kFwdWarps)
 render_fwd_kernel(KParams kp, const float4* __restrict__ recs, const int2* __restrict__ ranges,
-                  const int* __restrict__ point_list, const float4* __restrict__ streams,
+                  const int* __restrict__ point_list, int seg, const float4* __restrict__ streams,
                   const int* __restrict__ stream_count, int* __restrict__ stream_used, int W, int H,
                   int tiles_x, float bg0, float bg1, float bg2, float* __restrict__ image,
                   float* __restrict__ t_final, int* __restrict__ processed, int* __restrict__ contributors,
@@ -617,7 +708,11 @@ render_fwd_kernel(KParams kp, const float4* __restrict__ recs, const int2* __res
     px.nexact = 0;
 
     const float4* src = streams + kEntryVecs * stream_offset(tile, beg, end, warp);
-    const int n = stream_count[tile * kBlocksPerTile + warp];
+    const int n_culled = stream_count[tile * kBlocksPerTile + warp];
+    // While the stream can still grow (the cull kernel covered only the first `seg` entries of the
+    // list) only whole groups are composited here: the entries past the last whole group wait for
+    // forward_tail, which appends right behind them (there is no padding inside a stream).
+    const int n = (TAIL && end - beg > seg) ? n_culled - n_culled % kGroup : n_culled;
     const int nchunks = (n + kChunk - 1) / kChunk;
     float4* stage0 = ring[lwarp][0];
     unsigned long long* bar = bars[lwarp];
@@ -669,7 +764,7 @@ render_fwd_kernel(KParams kp, const float4* __restrict__ recs, const int2* __res
             }
             dead = !__any_sync(kFull, !(px.T < kTFloorF));
         }
-        used += g * kGroup;
+        used = c * kChunk + g * kGroup;  // the backward walks [0, used)
         __syncwarp();
         if (stage == kDepth - 1) {
             stage = 0;
@@ -692,6 +787,18 @@ render_fwd_kernel(KParams kp, const float4* __restrict__ recs, const int2* __res
             ++stage;
         }
     }
+    // Live pixels at the end of the stream and more of the list behind it: the block culls on by itself.
+    int n_stream = n_culled;            // entries of the stream, for exact_pixel below
+    int culled = (TAIL && end - beg > seg) ? seg : end - beg;
+    if (TAIL && culled < end - beg && c >= nchunks && __any_sync(kFull, !(px.T < kTFloorF))) {
+        const TailResult r = forward_tail<FAM>(kp, recs, point_list + beg, end - beg, culled, const_cast<float4*>(src),
+                                               n_stream, used, (float)bx + 0.5f, (float)by + 0.5f, fx, fy, lane, px);
+        px = r.px;
+        used = r.pos;
+        n_stream = r.n;
+        culled = r.culled;
+    }
+
     // Pixels whose transmittance came within the guard band of the floor: the last value (the first
     // below the floor, or the final one) and, for a pixel that crossed, the value just before the
     // crossing, recovered from the entry that crossed it.  FP32 cannot say on which entry such a
@@ -717,10 +824,18 @@ render_fwd_kernel(KParams kp, const float4* __restrict__ recs, const int2* __res
     }
     unsigned todo = kp.exact ? __ballot_sync(kFull, flagged) : 0u;
     const unsigned nfloor = __popc(__ballot_sync(kFull, flagged));
+    // the FP64 walk of a flagged pixel may go on past the entry its FP32 walk stopped at: it needs the
+    // survivors of the whole list
+    if (TAIL && todo) {
+        int done = culled;  // a local of this rare path: `culled` itself keeps out of memory
+        while (done < end - beg)
+            n_stream = extend_stream(kp, recs, point_list + beg, end - beg, done, const_cast<float4*>(src), n_stream,
+                                     (float)bx + 0.5f, (float)by + 0.5f, lane);
+    }
     while (todo) {
         const int l = __ffs(todo) - 1;
         todo &= todo - 1;
-        const ExactPixel ep = exact_pixel(kp, recs, src, n, end - beg, __shfl_sync(kFull, fx, l),
+        const ExactPixel ep = exact_pixel(kp, recs, src, n_stream, end - beg, __shfl_sync(kFull, fx, l),
                                           __shfl_sync(kFull, fy, l), lane);
         // the backward walks [0, used): it must reach the entry this pixel stopped on
         used = max(used, (ep.stream_end + kGroup - 1) & ~(kGroup - 1));
@@ -747,6 +862,7 @@ render_fwd_kernel(KParams kp, const float4* __restrict__ recs, const int2* __res
     if (lane == 0) {
         stream_used[tile * kBlocksPerTile + warp] = used;  // entries composited: all the backward needs
         atomicAdd(counters + CNT_COMPOSITED, (unsigned long long)used);
+        if (n_stream > n_culled) atomicAdd(counters + CNT_SURVIVORS, (unsigned long long)(n_stream - n_culled));
         if (nexact) atomicAdd(counters + CNT_EXACT, (unsigned long long)nexact);
         if (nfloor) atomicAdd(counters + CNT_TFLOOR, (unsigned long long)nfloor);
     }
@@ -1177,6 +1293,24 @@ darbs_status launch_pack(darbs_cuda_ctx* ctx, const KParams& kp, int64_t n, cons
 
 // Tests every list entry against the eight blocks of its tile and writes the per-block
 // survivor streams the render kernels consume.
+// How many entries of a tile's list the cull kernel covers before the forward takes over block by
+// block (forward_tail).  What a block needs is a saturation depth that belongs to the family, not to
+// the list: measured (scratch/seg_sweep.py, cull + forward in us, segment -> time):
+//   1 M splats 1080p   gaussian all 426, 512 484 | half-cosine-sq 256 222, all 290 |
+//                      raised-cosine all 309, 384 343 | inv-multiquadric 256 260, all 335
+//   3 M splats 4K      gaussian 384 1385, all 1866 | half-cosine-sq 128 710, 256 753, all 1661 |
+//                      raised-cosine 384 1212, all 1348 | inv-multiquadric 192 822, 256 864, all 1949
+// so: a base depth per family, applied when the mean list is at least 1.5 times as long (the tail
+// path reads its entries from global memory and is slower per visit than the stream walk).
+// ctx->cull_segment > 0 overrides (darbs_cuda_set_cull_segment).
+constexpr int kNoSegment = 1 << 30;
+int cull_segment(const darbs_cuda_ctx* ctx, const KParams& kp) {
+    if (ctx->cull_segment > 0) return ctx->cull_segment;
+    const int base = (kp.fam == FAM_HCOS2 || kp.fam == FAM_IMQ) ? 256 : 384;
+    const long long tiles = (long long)ctx->tiles_x * ctx->tiles_y;
+    return (tiles > 0 && 2 * ctx->fwd_entries >= 3 * (long long)base * tiles) ? base : kNoSegment;
+}
+
 darbs_status launch_cull(darbs_cuda_ctx* ctx, const KParams& kp) {
     const int tiles = ctx->tiles_x * ctx->tiles_y;
     if (tiles == 0) return DARBS_OK;
@@ -1186,7 +1320,8 @@ darbs_status launch_cull(darbs_cuda_ctx* ctx, const KParams& kp) {
     DARBS_TRY(reserve(ctx, ctx->stream_count, sizeof(int) * 2 * kBlocksPerTile * (size_t)tiles));
     cull_kernel<<<tiles, kThreads, 0, ctx->stream>>>(
         kp, (const float4*)ctx->recs.ptr, (const int2*)ctx->ranges.ptr, point_list_ptr(ctx), ctx->tiles_x,
-        (float4*)ctx->streams.ptr, (int*)ctx->stream_count.ptr, (unsigned long long*)ctx->counters.ptr);
+        cull_segment(ctx, kp), (float4*)ctx->streams.ptr, (int*)ctx->stream_count.ptr,
+        (unsigned long long*)ctx->counters.ptr);
     return check_launch(ctx, "cull_kernel");
 }
 
@@ -1201,10 +1336,18 @@ darbs_status launch_render_fwd(darbs_cuda_ctx* ctx, const KParams& kp, int width
     const int* plist = point_list_ptr(ctx);
     const int* count = (const int*)ctx->stream_count.ptr;
     int* used = (int*)ctx->stream_count.ptr + (size_t)kBlocksPerTile * tiles;
-#define DARBS_LAUNCH_FWD(F)                                                                       \
-    render_fwd_kernel<F><<<tiles * (kBlocksPerTile / kFwdWarps), 32 * kFwdWarps, 0, ctx->stream>>>(  \
-        kp, recs, ranges, plist, (const float4*)ctx->streams.ptr, count, used, width, height,     \
+    const int seg = cull_segment(ctx, kp);
+#define DARBS_LAUNCH_FWD_(F, T)                                                                      \
+    render_fwd_kernel<F, T><<<tiles * (kBlocksPerTile / kFwdWarps), 32 * kFwdWarps, 0, ctx->stream>>>(  \
+        kp, recs, ranges, plist, seg, (const float4*)ctx->streams.ptr, count, used, width, height,     \
         ctx->tiles_x, bg[0], bg[1], bg[2], image, t_final, processed, contributors, counters)
+#define DARBS_LAUNCH_FWD(F)              \
+    do {                                 \
+        if (seg < kNoSegment)            \
+            DARBS_LAUNCH_FWD_(F, true);  \
+        else                             \
+            DARBS_LAUNCH_FWD_(F, false); \
+    } while (0)
     switch (kp.fam) {
         case FAM_GAUSS2: DARBS_LAUNCH_FWD(FAM_GAUSS2); break;
         case FAM_HCOS2: DARBS_LAUNCH_FWD(FAM_HCOS2); break;
@@ -1213,6 +1356,7 @@ darbs_status launch_render_fwd(darbs_cuda_ctx* ctx, const KParams& kp, int width
         case FAM_MSINC1: DARBS_LAUNCH_FWD(FAM_MSINC1); break;
         default: DARBS_LAUNCH_FWD(FAM_GENERIC); break;
     }
+#undef DARBS_LAUNCH_FWD_
 #undef DARBS_LAUNCH_FWD
     return check_launch(ctx, "render_fwd_kernel");
 }

@@ -232,6 +232,38 @@ def test_forward_and_backward_parity_needle_splats(ctx, port, name):
     assert grad_err(got, ref_g).max() <= 5.0 * GRAD_TOL
 
 
+@pytest.mark.parametrize("name", ["gaussian", "half-cosine-sq", "inv-multiquadratic", "custom:raised-cosine:1.0:0.6:2"])
+def test_results_do_not_depend_on_the_cull_segment(ctx, port, name):
+    """The cull kernel may cover only the first entries of every tile's list; blocks whose pixels
+    outlive them cull on inside the forward (render.cu forward_tail).  Whatever the segment, the
+    per-pixel walk is the reference's (rasterizer.cpp:85-107): integer aux equal to the oracle's,
+    images equal among themselves, gradients within tolerance."""
+    k = oracle_kernel(port, name)
+    n, w, h = 20000, 128, 96  # ~300 entries per tile
+    s = port.random_scene(k, n, w, h, 17)
+    s.opacity[:] = f32(np.random.default_rng(3).uniform(0.02, 0.3, n))  # slow saturation: long walks
+    g = port.random_image_grad(w, h, 4)
+    fr = port.forward(k, s, w, h, BG, threads=0, keep=True)
+    st, ref_g = port.backward(fr["handle"], k, g, s, threads=0)
+    port.forward_free(fr["handle"])
+    sc = scene_f32(s)
+    images = []
+    try:
+        for seg in (1 << 30, 8, 40, 96, 200):
+            ctx.set_cull_segment(seg)
+            out = ctx.forward(gpu_kernel_cached(name), **sc, width=w, height=h, background=BG)
+            assert np.array_equal(out["processed"], fr["processed"]), seg
+            assert np.array_equal(out["contributors"], fr["contributors"]), seg
+            assert np.abs(out["image"] - fr["image"]).max() <= IMG_TOL
+            images.append(out["image"].copy())
+            got = ctx.backward(gpu_kernel_cached(name), f32(g), n)
+            assert grad_err(got, ref_g).max() <= GRAD_TOL, seg
+    finally:
+        ctx.set_cull_segment(0)
+    for img in images[1:]:
+        assert np.abs(img - images[0]).max() <= 1e-6
+
+
 def test_transmittance_floor_pixels_are_exact(ctx, port):
     """The last decision of a pixel, T < 1e-4 (rasterizer.cpp:100), cannot be taken in FP32 when T
     ends within a few 1e-9 of the floor: the forward kernel composites those pixels again in FP64
