@@ -268,7 +268,10 @@ DARBS_API darbs_status darbs_cuda_set_accumulate(darbs_cuda_ctx* ctx, int accumu
  * pointer as `target` with image_space = DARBS_HOST.  The transfer is queued on the context's
  * copy stream behind the cull kernel of the last view queued, i.e. it runs under that view's
  * render kernels.  Two uploads may be outstanding; the image must not change until its
- * evaluate_view has been queued.  Without a prefetch evaluate_view uploads the image itself. */
+ * evaluate_view has been queued, and a staged image is recognised by its host POINTER alone: do not
+ * free the buffer and reuse its address for another image between the two calls.  A second prefetch
+ * into a slot waits for the loss kernels that read the slot's previous image.  Without a prefetch
+ * evaluate_view uploads the image itself. */
 DARBS_API darbs_status darbs_cuda_prefetch_target(darbs_cuda_ctx* ctx, const float* host_image,
                                                   int64_t count);
 

@@ -638,22 +638,31 @@ template <int FAM>
 __device__ __noinline__ TailResult forward_tail(const KParams& kp, const float4* __restrict__ recs,
                                                 const int* __restrict__ list, int list_len, int culled,
                                                 float4* __restrict__ dst, int n, int pos, float bx05, float by05,
-                                                float fx, float fy, int lane, FwdPixel px) {
+                                                float fx, float fy, int lane, FwdPixel px, float4* __restrict__ smem,
+                                                int smem_entries) {
     constexpr int kGroup = FwdGroup<FAM>::value;
     bool dead = false;
     while (true) {
         const bool last_round = culled >= list_len;
         const int n_run = last_round ? n : n - n % kGroup;  // the last group may run into the null padding
-        for (; pos < n_run && !dead; pos += kGroup) {
-            const float4* qb = dst + (size_t)pos * kEntryVecs;
-            const FwdPixel save = px;
-            bool near_acc = false;
-            for (int j = 0; j < kGroup; ++j) fwd_visit<FAM, false, true>(kp, recs, qb + j * 3, fx, fy, px, near_acc);
-            if (kp.exact && __any_sync(kFull, near_acc)) {
-                px = save;
-                for (int j = 0; j < kGroup; ++j) fwd_visit<FAM, true, true>(kp, recs, qb + j * 3, fx, fy, px, near_acc);
+        while (pos < n_run && !dead) {
+            // the warp's ring is idle here: the next entries are staged in it by plain copies (the warp
+            // wrote them itself a moment ago), so a visit reads shared memory as in the stream walk
+            const int batch = min(((n_run - pos + kGroup - 1) / kGroup) * kGroup, smem_entries);
+            __syncwarp();
+            for (int i = lane; i < batch * kEntryVecs; i += 32) smem[i] = dst[(size_t)pos * kEntryVecs + i];
+            __syncwarp();
+            for (int b = 0; b < batch && !dead; b += kGroup, pos += kGroup) {
+                const float4* qb = smem + b * kEntryVecs;
+                const FwdPixel save = px;
+                bool near_acc = false;
+                for (int j = 0; j < kGroup; ++j) fwd_visit<FAM, false, true>(kp, recs, qb + j * 3, fx, fy, px, near_acc);
+                if (kp.exact && __any_sync(kFull, near_acc)) {
+                    px = save;
+                    for (int j = 0; j < kGroup; ++j) fwd_visit<FAM, true, true>(kp, recs, qb + j * 3, fx, fy, px, near_acc);
+                }
+                dead = !__any_sync(kFull, !(px.T < kTFloorF));
             }
-            dead = !__any_sync(kFull, !(px.T < kTFloorF));
         }
         if (dead || last_round) break;
         n = extend_stream(kp, recs, list, list_len, culled, dst, n, bx05, by05, lane);
@@ -792,7 +801,8 @@ render_fwd_kernel(KParams kp, const float4* __restrict__ recs, const int2* __res
     int culled = (TAIL && end - beg > seg) ? seg : end - beg;
     if (TAIL && culled < end - beg && c >= nchunks && __any_sync(kFull, !(px.T < kTFloorF))) {
         const TailResult r = forward_tail<FAM>(kp, recs, point_list + beg, end - beg, culled, const_cast<float4*>(src),
-                                               n_stream, used, (float)bx + 0.5f, (float)by + 0.5f, fx, fy, lane, px);
+                                               n_stream, used, (float)bx + 0.5f, (float)by + 0.5f, fx, fy, lane, px,
+                                               stage0, kDepth * kChunk);
         px = r.px;
         used = r.pos;
         n_stream = r.n;

@@ -647,19 +647,15 @@ inline Fit3DResult fit_scene(const std::vector<View>& views, const KernelSpec& k
         for (int k = 0; k < kParamsPerPrim; ++k) q[k] = params[i * kParamsPerPrim + k];
         result.primitives[i] = realize(q);
     }
-    // final metrics (fit3d.cpp:187-198): one more evaluation without gradients gives per-view
-    // mse and dssim of the fitted scene
+    // final metrics (fit3d.cpp:187-198): the fitted scene rendered per view by the non-throwing
+    // render_scene (a view that sees nothing is a background image there, not an error)
     double mse_sum = 0.0, ssim_sum = 0.0;
     for (std::size_t v = 0; v < views.size(); ++v) {
-        double out[4];
-        throw_status(darbs_cuda_evaluate_view(ctx, &ks, psi, (int64_t)n, d_params.data(), blocks[v].data(), bg,
-                                              d_targets[v].data(), 1.0, nullptr, nullptr, nullptr, out, DARBS_DEVICE,
-                                              DARBS_DEVICE),
-                     ctx);
-        result.per_view_psnr.push_back(out[3] <= 0.0 ? std::numeric_limits<double>::infinity()
-                                                     : -10.0 * std::log10(out[3]));
-        mse_sum += out[3];
-        ssim_sum += 1.0 - 2.0 * out[2];
+        const ImageBuffer img = render_scene(result.primitives, views[v].camera, kernel, psi, Vec3::Zero(), config.threads);
+        const double m = mse(img, views[v].target);
+        result.per_view_psnr.push_back(m <= 0.0 ? std::numeric_limits<double>::infinity() : -10.0 * std::log10(m));
+        mse_sum += m;
+        ssim_sum += ssim(img, views[v].target);
     }
     const double nv = double(views.size());
     result.report.final_mse = mse_sum / nv;
