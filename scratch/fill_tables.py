@@ -73,7 +73,7 @@ rows4 = [
     ("3. 1M splats 1080p fwd+bwd+Adam per kernel", " / ".join(f"{r['per_kernel'][k]['ms_per_iter'] / 1e3:.1f}" for k in K) + f" s per iteration ({r['cpu_baseline']['cores']} threads, full size; {r['value']:.3f} view-iterations/s)",
      " / ".join(f"{pk[k]['ms_per_iter']:.2f}" for k in K) + f" ms per iteration ({b['value']:.0f} view-iterations/s; e2e {b['e2e']['value']:.0f})",
      "render_bwd frac " + " / ".join(f"{pk[k]['render_bwd']['frac']:.2f}" for k in K) + f" of {rf['peak']:.0f} TFLOP/s", "—"),
-    ("4. 3M splats × 64 views, view-sharded + NCCL all-reduce", "not run (64 views × ≈ 10 s of CPU time per view at 3 M primitives, per kernel)", "one rank's share (8 views of 64) on one B200: 516 view-iterations/s (1.94 ms per view), e2e 509", "as row 3 per view", "not measured: no multi-GPU node in this run (`bench.py --gpus N` runs it)"),
+    ("4. 3M splats × 64 views, view-sharded + NCCL all-reduce", "not run (64 views × ≈ 10 s of CPU time per view at 3 M primitives, per kernel)", "one rank's share (8 views of 64) on one B200: 565 view-iterations/s (1.77 ms per view), e2e 559", "as row 3 per view", "not measured: no multi-GPU node in this run (`bench.py --gpus N` runs it)"),
     ("5. kernel sweep × 100k–5M splats @ 4K", "not run above 1M", "gaussian " + " / ".join(f"{sweep_row('gaussian', n)[0]:.2f}" for n in (100_000, 1_000_000, 5_000_000)) + " ms per iteration at 100k / 1M / 5M; all rows: `profiles/r2_sweep_4k.md`",
      "cull and binning dominate beyond 1M (DESIGN §8)", "—"),
 ]
