@@ -138,3 +138,29 @@ def test_two_ranks_match_the_serial_view_loop(tmp_path):
     assert np.abs(r0["params"] - ref_p).max() <= 1e-9
     assert np.abs(r0["losses"] - ref_l).max() <= 1e-12
     assert np.abs(ref_p - _setup()[0]).max() > 1e-5  # the steps did move the parameters
+
+
+def test_four_ranks_with_uneven_view_counts(tmp_path):
+    """World size 4 over 5 views: ranks own 2, 1, 1, 1 views (view v -> rank v mod 4), one rank more
+    than the others; the all-reduce is a SUM without any per-rank weight, so the result is still the
+    serial loop's (fit3d.cpp:148-158 sums the views; :161-165 divides the loss by the view count)."""
+    import torch.multiprocessing as mp
+
+    steps, world = 2, 4
+    port = _free_port()
+    mp.spawn(_worker, args=(world, port, steps, str(tmp_path)), nprocs=world, join=True)
+    ref_p, ref_l = _serial(steps)
+    ranks = [np.load(tmp_path / f"rank{r}.npz") for r in range(world)]
+    assert [r["views"].tolist() for r in ranks] == [[0, 4], [1], [2], [3]]
+    for r in ranks[1:]:
+        assert np.array_equal(r["params"], ranks[0]["params"])
+        assert np.array_equal(r["losses"], ranks[0]["losses"])
+    assert np.abs(ranks[0]["params"] - ref_p).max() <= 1e-9
+    assert np.abs(ranks[0]["losses"] - ref_l).max() <= 1e-12
+
+
+def test_more_ranks_than_views_leaves_idle_ranks_consistent(tmp_path):
+    """A rank without a view contributes zeros to the sum and still ends with the same parameters."""
+    from paper_2501_12369_b200.multiview import local_views
+
+    assert local_views(N_VIEWS, 8, 6) == [] and local_views(N_VIEWS, 8, 4) == [4]
