@@ -373,7 +373,7 @@ def run_ours(args):
             ctx.adam_step(s["params"].view(-1), s["grads"].view(-1), s["m"], s["v"], lrs, s["t"])
         if e2e:
             pending[0] += 1
-            if pending[0] > 1:  # the previous iteration's loss, now that this one is queued
+            if pending[0] > 2:  # the loss of two iterations ago: the host stays a full iteration ahead of the read-back
                 losses.append(ctx.pop_loss())
                 pending[0] -= 1
         return loss

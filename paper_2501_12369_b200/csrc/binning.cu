@@ -401,7 +401,8 @@ darbs_status binning_begin(darbs_cuda_ctx* ctx, int64_t n, int width, int height
     const int tiles = ctx->tiles_x * ctx->tiles_y;
     if (ctx->tiles_x > 65535 || ctx->tiles_y > 65535)
         return fail(ctx, DARBS_INVALID_PARAMETER, "image too large for 16-bit tile coordinates");
-    if (n >= (int64_t)1 << 31) return fail(ctx, DARBS_INVALID_PARAMETER, "too many splats");
+    // the sort's look-back words carry 30-bit counts (radix.cuh)
+    if (n >= (int64_t)1 << 30) return fail(ctx, DARBS_INVALID_PARAMETER, "too many splats (2^30 or more)");
 
     DARBS_TRY(reserve(ctx, ctx->ranges, sizeof(int2) * (size_t)(tiles > 0 ? tiles : 1)));
     DARBS_CUDA_TRY(ctx, cudaMemsetAsync(ctx->ranges.ptr, 0, sizeof(int2) * (size_t)tiles, s));
