@@ -218,6 +218,25 @@ def reference_table(args):
                 tb += (t2 - t1) / 3
         rows[f"{th}_threads"] = {"ms_forward": 1e3 * tf, "ms_backward": 1e3 * tb}
     out["config0_10k_256_half-cosine-sq"] = rows
+    # the reference's own micro-benchmark sizes (benchmarks/bench.cpp:58-75, 116-117): 200 / 1000 splats, 128 x 128, Gaussian
+    kg = orc.preset("gaussian")
+    small = {}
+    for n_small in (200, 1000):
+        sc = orc.random_scene(kg, n_small, 128, 128, 7)
+        g1 = np.ones((128, 128, 3))
+        tf = tb = 0.0
+        for rep in range(12):
+            t0 = time.perf_counter()
+            fr = orc.forward(kg, sc, 128, 128, (0.1, 0.2, 0.3), threads=1, keep=True)
+            t1 = time.perf_counter()
+            orc.backward(fr["handle"], kg, g1, sc, threads=1)
+            t2 = time.perf_counter()
+            orc.forward_free(fr["handle"])
+            if rep >= 2:
+                tf += (t1 - t0) / 10
+                tb += (t2 - t1) / 10
+        small[f"{n_small}_splats_128x128_gaussian"] = {"us_forward": 1e6 * tf, "us_backward": 1e6 * tb, "threads": 1}
+    out["bm_forward_backward"] = small
     truth = syn.scene_b(args.splats, 1)
     cam = syn.orbit_camera(0, 1, args.width, args.height, args.focal)
     fwd = {}
@@ -688,7 +707,7 @@ def run_config3(args):
     bg = (0.0, 0.0, 0.0)
     kernels = {name: (darbs.kernel_preset(name), darbs.default_psi(name)) for name in KERNELS}
 
-    def make_state(views):
+    def make_state(views, with_hosts=True):
         st = {}
         for name, (k, psi) in kernels.items():
             targets, hosts = [], []
@@ -696,7 +715,8 @@ def run_config3(args):
                 t = torch.empty((h, w, 3), dtype=torch.float32, device=dev)
                 ctx.evaluate_view(k, psi, truth_d, cams[v], bg, grad_image=torch.zeros_like(t), image_out=t)
                 targets.append(t)
-                hosts.append(t.cpu().pin_memory().numpy())
+                if with_hosts:  # the end-to-end leg's pinned copies (25 MB per view and kernel)
+                    hosts.append(t.cpu().pin_memory().numpy())
             st[name] = dict(params=torch.from_numpy(init).to(dev).clone(), m=torch.zeros(14 * n, device=dev),
                             v=torch.zeros(14 * n, device=dev), grads=torch.zeros((n, 14), device=dev),
                             targets=targets, hosts=hosts, views=list(views), t=0)
@@ -805,7 +825,7 @@ def run_config3(args):
             ctx.comm_destroy()
             del state
             torch.cuda.empty_cache()
-            full = make_state(range(V))
+            full = make_state(range(V), with_hosts=False)
             for name in KERNELS:
                 iteration(full, name, False)
             steps1 = min(args.steps, 2)

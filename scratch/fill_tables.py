@@ -31,7 +31,8 @@ rows = [
      f"{dr['value']:.0f} pairs/s; forward " + " / ".join(f"{dr['per_kernel'][k]['ms_forward']:.1f}" for k in K) + " ms, backward "
      + " / ".join(f"{dr['per_kernel'][k]['ms_backward']:.1f}" for k in K) + " ms (PCIe: 69 MB in, 86 MB out per pair)"),
     ("small-scene latency through the same host-array calls (the reference's `bm_forward` / `bm_backward` sizes, 128², Gaussian)",
-     "; ".join(f"{k.split('_')[0]} splats: forward {v['us_forward']:.0f} µs, backward {v['us_backward']:.0f} µs" for k, v in dr["small_scene_latency"].items())),
+     "; ".join(f"{k.split('_')[0]} splats: forward {v['us_forward']:.0f} µs, backward {v['us_backward']:.0f} µs" for k, v in dr["small_scene_latency"].items())
+     + (" — the reference's CPU code, one thread, same sizes: " + "; ".join(f"{k.split('_')[0]} splats: {v['us_forward'] / 1e3:.1f} ms / {v['us_backward'] / 1e3:.1f} ms" for k, v in t["bm_forward_backward"].items()) if "bm_forward_backward" in t else "")),
     (f"`roofline` (dominant kernel `{rf['kernel']}`, {pk['gaussian']['render_bwd']['ms']:.3f} ms)",
      f"{rf['achieved']:.1f} TFLOP/s algorithmic of {rf['peak']:.1f} measured (FFMA2; scalar FFMA {rf['peak_ffma_tflops']:.1f}): `frac` **{rf['frac']:.2f}**; `frac_evaluated` {rf['frac_evaluated']:.2f}; "
      f"DRAM traffic {rf['traffic'] / 1e6:.0f} MB per launch; SM clock {rf['peak_sm_mhz']:.0f} MHz"),
