@@ -83,6 +83,21 @@ def test_bins_more_than_65536_tiles(ctx, port):
     check_bins(ctx, port, s, w, h)
 
 
+@pytest.mark.parametrize("shape,n", [((16, 400), 900), ((400, 16), 900), ((16, 16), 300), ((4112, 48), 4000),
+                                     ((48, 4112), 4000), ((1920, 1080), 60000)])
+def test_bins_every_digit_plan(ctx, port, shape, n):
+    """The tile sort runs one radix pass per coordinate byte that can differ (binning.cu tile_plan): a
+    single tile column or row drops that coordinate's pass, a single tile needs no pass, more than
+    256 columns or rows switch to 32-bit keys with a second byte; the expand kernel's per-splat digit
+    histograms take the byte-digit shortcut only for the two-pass 16-bit case.  Also a list long
+    enough for several chunks of the 8192-pair passes and of the 2048-rank expand CTAs."""
+    w, h = shape
+    k = port.preset("half-cosine-sq")
+    s = port.random_scene(k, n, w, h, 23)
+    s.radius[:4] = 300.0  # a few splats across many tiles
+    check_bins(ctx, port, s, w, h)
+
+
 def test_bins_equal_depth_index_order(ctx, port):
     """Equal depths are ordered by splat index, test_rasterizer.cpp:84-94."""
     k = port.preset("gaussian")
