@@ -127,6 +127,39 @@ def test_port_reproduces_loss_golden(port):
 
 
 # ----------------------------------------------------------------------------- GPU: the C ABI
+@pytest.mark.parametrize("name", ["gaussian", "half-cosine-sq", "raised-cosine", "mod-sinc", "inv-multiquadratic"])
+def test_port_reproduces_the_first_iteration_of_the_reference_fit(port, name):
+    """tests/golden/fit.npz holds the reference's own fit_scene runs on its demo scene (made by
+    make_golden.py through oracle/_ref).  Its first recorded loss is fit3d.cpp:108-165 evaluated at the
+    stored start: the port's project -> forward -> loss_total over the four demo cameras must give
+    the same mean (this pins the fixture the GPU drivers are compared with, without a GPU), and the
+    port's render of the truth must be the stored reference render."""
+    z = np.load(os.path.join(GOLD, "fit.npz"))
+    k, psi = port.preset(name), port.default_psi(name)
+    cams, truth, init = z["cameras"], z["truth"], z["init_0.02"]
+    sums = np.zeros(3)
+    for v, cam in enumerate(cams):
+        w, h = int(cam[4]), int(cam[5])
+
+        def render(prims):
+            st, pr = port.project(k, psi, prims, cam)
+            assert st == 0
+            vis = np.flatnonzero(pr["valid"])
+            s = Scene(pr["mu2"][vis], None, pr["conic"][vis], pr["radius"][vis], pr["depth"][vis], prims[vis, 10],
+                      prims[vis, 11:14])
+            return port.forward(k, s, w, h, (0, 0, 0), threads=0)["image"]
+
+        ref_render = z[f"{name}/render"][v]
+        assert np.abs(render(truth) - ref_render).max() <= 1e-12
+        target = ref_render.astype(np.float32).astype(np.float64)  # the float32 dumps both sides read
+        st, vals, _ = port.loss_total(render(init), target, 0.2, want_grad=False)
+        sums += vals
+    mean = sums / len(cams)
+    assert abs(mean[0] - z[f"{name}/fit50/loss"][0]) <= 1e-12
+    assert abs(mean[1] - z[f"{name}/fit50/l1"][0]) <= 1e-12
+    assert abs(mean[2] - z[f"{name}/fit50/dssim"][0]) <= 1e-12
+
+
 @pytest.mark.gpu
 @pytest.mark.parametrize("path", RASTER, ids=ident)
 def test_gpu_reproduces_raster_golden(ctx, darbs, path):
