@@ -118,6 +118,17 @@ DARBS_API darbs_status darbs_cuda_set_exact_decisions(darbs_cuda_ctx* ctx, int e
  * associative, so the result is bitwise independent of the order in which blocks arrive and a
  * rerun is bitwise identical.  0: float32 vector reductions (faster; equal up to summation order). */
 DARBS_API darbs_status darbs_cuda_set_deterministic(darbs_cuda_ctx* ctx, int enabled);
+/* evaluate_view / train_step normally wait (an event, not the stream) for ONE number of a view,
+ * K = the total of tile entries, to size the entry buffers.  A caller that knows a bound — a
+ * training loop whose previous iterations saw K_prev can pass 1.25 K_prev — sets it here
+ * (entries > 0) and the wait disappears: buffers and grids are sized by the capacity, the kernels
+ * take K from the device, and an iteration can be queued without any host synchronisation
+ * (CUDA-graph capturable).  A view with K > capacity is TRUNCATED safely (no write leaves the
+ * buffers) and reported as DARBS_CONTRACT_VIOLATION by the call that collects its loss
+ * (darbs_cuda_pop_loss, or evaluate_view / train_step with loss_out).  0 restores the wait.
+ * Heuristics that look at K (the cull segment) take the capacity to be 1.25 x the expected K.
+ * Only the fused training path honours it; darbs_cuda_forward / darbs_cuda_bin always wait. */
+DARBS_API darbs_status darbs_cuda_set_entry_capacity(darbs_cuda_ctx* ctx, int64_t entries);
 /* Tuning knob without a reference analogue.  The cull kernel tests only the first `entries` list
  * entries of every tile against its eight 8x4 pixel blocks; a block whose pixels are still live
  * behind them culls on by itself inside the forward kernel.  Results do not depend on the value

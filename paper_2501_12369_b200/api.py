@@ -84,6 +84,7 @@ def _load():
     lib.darbs_cuda_set_exact_decisions.argtypes = [vp, i32]
     lib.darbs_cuda_set_deterministic.argtypes = [vp, i32]
     lib.darbs_cuda_set_cull_segment.argtypes = [vp, i32]
+    lib.darbs_cuda_set_entry_capacity.argtypes = [vp, i64]
     lib.darbs_cuda_make_kernel.argtypes = [i32, dbl, dbl, i32, ks]
     lib.darbs_cuda_kernel_preset.argtypes = [C.c_char_p, ks]
     lib.darbs_cuda_default_psi.argtypes = [C.c_char_p]
@@ -125,7 +126,7 @@ _lib = _load()
 
 EXPORTED_SYMBOLS = (
     "darbs_cuda_version darbs_cuda_create darbs_cuda_destroy darbs_cuda_last_error darbs_cuda_set_stream "
-    "darbs_cuda_synchronize darbs_cuda_launch_count darbs_cuda_set_exact_decisions darbs_cuda_set_deterministic darbs_cuda_set_cull_segment darbs_cuda_make_kernel "
+    "darbs_cuda_synchronize darbs_cuda_launch_count darbs_cuda_set_exact_decisions darbs_cuda_set_deterministic darbs_cuda_set_cull_segment darbs_cuda_set_entry_capacity darbs_cuda_make_kernel "
     "darbs_cuda_kernel_preset darbs_cuda_default_psi darbs_cuda_eval darbs_cuda_bin darbs_cuda_forward "
     "darbs_cuda_backward darbs_cuda_realize darbs_cuda_project darbs_cuda_backward_projection "
     "darbs_cuda_evaluate_view darbs_cuda_prefetch_target darbs_cuda_pop_loss darbs_cuda_adam_step darbs_cuda_set_stage_timing darbs_cuda_stage_times "
@@ -302,6 +303,11 @@ class Context:
     def set_deterministic(self, enabled: bool):
         """Order-independent fixed-point accumulation of gradients and loss sums (bitwise repeatable)."""
         self._check(_lib.darbs_cuda_set_deterministic(self._h, int(bool(enabled))))
+
+    def set_entry_capacity(self, entries: int):
+        """Promise K <= entries for the following evaluate_view / train_step calls: they stop waiting for K
+        (0 restores the wait).  A view that breaks the promise raises contract_violation when its loss is collected."""
+        self._check(_lib.darbs_cuda_set_entry_capacity(self._h, int(entries)))
 
     def set_cull_segment(self, entries: int):
         """List entries per tile the cull kernel covers before the forward extends streams by itself (0: default)."""

@@ -893,6 +893,14 @@ darbs_status darbs_cuda_evaluate_view(darbs_cuda_ctx* ctx, const darbs_kernel_sp
     return DARBS_OK;
 }
 
+darbs_status darbs_cuda_set_entry_capacity(darbs_cuda_ctx* ctx, int64_t entries) {
+    CTX_OR_FAIL(ctx);
+    if (entries < 0 || entries >= ((int64_t)1 << 30))
+        return fail(ctx, DARBS_INVALID_PARAMETER, "set_entry_capacity: negative or 2^30 and more");
+    ctx->entry_capacity = entries;
+    return DARBS_OK;
+}
+
 darbs_status darbs_cuda_set_cull_segment(darbs_cuda_ctx* ctx, int entries) {
     CTX_OR_FAIL(ctx);
     if (entries < 0) return fail(ctx, DARBS_INVALID_PARAMETER, "set_cull_segment: negative");
@@ -959,6 +967,11 @@ darbs_status darbs_cuda_pop_loss(darbs_cuda_ctx* ctx, double loss_out[4]) {
     }
     if (loss_out)
         for (int i = 0; i < 4; ++i) loss_out[i] = out[i];
+    unsigned long long overflow;
+    std::memcpy(&overflow, (const char*)slot.host + 8, 8);
+    if (overflow)
+        return fail(ctx, DARBS_CONTRACT_VIOLATION,
+                    "evaluate_view: more tile entries than darbs_cuda_set_entry_capacity promised; the view is incomplete");
     if (flags[0] & 1) return fail(ctx, DARBS_INVALID_PARAMETER, "covariance_from_scale_rot: scale must be positive");
     if (flags[0] & 2) return fail(ctx, DARBS_NUMERIC_ERROR, "conic_and_radius: covariance not positive definite");
     if (flags[1] == 0) return fail(ctx, DARBS_NUMERIC_ERROR, "fit_scene: all primitives culled in one view");
@@ -1062,8 +1075,10 @@ darbs_status darbs_cuda_work_counters(darbs_cuda_ctx* ctx, int64_t out[8]) {
     DARBS_CUDA_TRY(ctx, cudaMemcpyAsync(ctx->pinned, c, sizeof(unsigned long long) * 8,
                                         cudaMemcpyDeviceToHost, ctx->stream));
     DARBS_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+    unsigned long long total = 0;  // K as the device counted it (the host may only know a capacity)
+    DARBS_CUDA_TRY(ctx, cudaMemcpy(&total, c + 8, sizeof(total), cudaMemcpyDeviceToHost));
     for (int i = 0; i < 8; ++i) out[i] = (int64_t)((unsigned long long*)ctx->pinned)[i];
-    out[0] = ctx->fwd_entries;
+    out[0] = (int64_t)total;
     return DARBS_OK;
 }
 

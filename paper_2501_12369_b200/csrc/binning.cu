@@ -98,7 +98,7 @@ __global__ void __launch_bounds__(kExpandThreads)
 expand_kernel(unsigned n, const unsigned* __restrict__ order, const uint2* __restrict__ rects,
               const unsigned* __restrict__ touched, radix::Plan plan, unsigned* __restrict__ hist,
               unsigned* __restrict__ status, unsigned* __restrict__ ticket, TileKey* __restrict__ tile_keys,
-              unsigned* __restrict__ tile_vals) {
+              unsigned* __restrict__ tile_vals, unsigned capacity, unsigned long long* __restrict__ overflow) {
     using Pack = TilePack<TileKey>;
     __shared__ unsigned s_hist[radix::kMaxPasses * radix::kBins];
     __shared__ unsigned s_wtot[kExpandThreads / 32];
@@ -241,7 +241,7 @@ expand_kernel(unsigned n, const unsigned* __restrict__ order, const uint2* __res
             const unsigned o_idx = __shfl_sync(full, idx[i], lo);
             const unsigned rx = __shfl_sync(full, rect[i].x, lo), ry = __shfl_sync(full, rect[i].y, lo);
             const unsigned x0 = rx & 0xffffu, y0 = rx >> 16, w = (ry & 0xffffu) - x0 + 1u;
-            if (e < total) {
+            if (e < total && base + e < capacity) {  // capacity: what the entry buffers were sized for
                 const unsigned q = e - o_rel;
                 const unsigned qy = q / w, qx = q - qy * w;
                 tile_keys[base + e] = Pack::pack(x0 + qx, y0 + qy);
@@ -250,16 +250,23 @@ expand_kernel(unsigned n, const unsigned* __restrict__ order, const uint2* __res
         }
         base += total;
     }
+    // more entries than the caller's capacity (darbs_cuda_set_entry_capacity): the view is incomplete
+    if (tid == 0 && (unsigned long long)s_base + cta_total > capacity) *overflow = 1ull;
     __syncthreads();
     for (int i = tid; i < plan.passes * radix::kBins; i += kExpandThreads)
         if (s_hist[i]) atomicAdd(&hist[i], s_hist[i]);
 }
 
 template <typename TileKey>
-__global__ void ranges_kernel(int64_t k, const TileKey* __restrict__ sorted_tiles, int tiles_x,
-                              int2* __restrict__ ranges) {
+__global__ void ranges_kernel(int64_t k_bound, const unsigned long long* __restrict__ k_dev,
+                              const TileKey* __restrict__ sorted_tiles, int tiles_x, int2* __restrict__ ranges) {
     // eight consecutive entries per thread: one boundary test per entry against its predecessor
     constexpr int kPer = 8;
+    int64_t k = k_bound;  // or the count on the device; beyond the bound nothing was sorted: no ranges
+    if (k_dev) {
+        if (*k_dev > (unsigned long long)k_bound) return;
+        k = (int64_t)*k_dev;
+    }
     const int64_t first = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) * kPer;
     if (first >= k) return;
     unsigned prev = first > 0 ? TilePack<TileKey>::tile_of(sorted_tiles[first - 1], tiles_x) : 0xffffffffu;
@@ -357,8 +364,9 @@ radix::Plan tile_plan(int tiles_x, int tiles_y) {
 // expand kernel's status words) was cleared by binning_begin; the status words of the tile passes
 // depend on K and are cleared here.
 template <typename TileKey>
-darbs_status tile_sort(darbs_cuda_ctx* ctx, int64_t n, int64_t k, const unsigned* order, const uint2* rects,
-                       const unsigned* touched) {
+// k: the entry count, or (k_dev given) the capacity the caller vouches for while the count stays on the device.
+darbs_status tile_sort(darbs_cuda_ctx* ctx, int64_t n, int64_t k, const unsigned long long* k_dev,
+                       const unsigned* order, const uint2* rects, const unsigned* touched) {
     cudaStream_t s = ctx->stream;
     DARBS_TRY(reserve(ctx, ctx->tile_keys, sizeof(unsigned) * 2 * (size_t)k));  // sized for 32-bit keys
     DARBS_TRY(reserve(ctx, ctx->tile_vals, sizeof(unsigned) * 2 * (size_t)k));
@@ -375,20 +383,23 @@ darbs_status tile_sort(darbs_cuda_ctx* ctx, int64_t n, int64_t k, const unsigned
 
     // pass 0 = the column byte, pass 1 = the row byte: the histograms need neither shifts nor masks
     const bool byte_digits = sizeof(TileKey) == 2 && plan.passes == 2 && plan.shift[1] == 8;
+    unsigned long long* overflow = (unsigned long long*)ctx->counters.ptr + kOverflowAt;
     if (byte_digits)
         expand_kernel<TileKey, true><<<grid_for(n, kExpandChunk), kExpandThreads, 0, s>>>(
-            (unsigned)n, order, rects, touched, plan, ws.tile_hist, ws.expand_status, ws.expand_ticket, tk0, tv0);
+            (unsigned)n, order, rects, touched, plan, ws.tile_hist, ws.expand_status, ws.expand_ticket, tk0, tv0,
+            (unsigned)k, overflow);
     else
         expand_kernel<TileKey, false><<<grid_for(n, kExpandChunk), kExpandThreads, 0, s>>>(
-            (unsigned)n, order, rects, touched, plan, ws.tile_hist, ws.expand_status, ws.expand_ticket, tk0, tv0);
+            (unsigned)n, order, rects, touched, plan, ws.tile_hist, ws.expand_status, ws.expand_ticket, tk0, tv0,
+            (unsigned)k, overflow);
     DARBS_TRY(check_launch(ctx, "expand_kernel"));
     DARBS_CUDA_TRY(ctx, radix::launch_passes<TileKey>(tk0, tv0, tk1, tv1, (unsigned)k, plan, ws.tile_tickets,
-                                                      ws.tile_hist, (unsigned*)ctx->tile_status.ptr, s));
+                                                      ws.tile_hist, (unsigned*)ctx->tile_status.ptr, s, k_dev));
     ctx->launches += plan.passes;
     ctx->cur_key_buf = plan.passes & 1;
     const TileKey* sorted_tiles = ctx->cur_key_buf ? tk1 : tk0;
-    ranges_kernel<TileKey><<<grid_for(((int64_t)k + 7) / 8, 256), 256, 0, s>>>((int64_t)k, sorted_tiles, ctx->tiles_x,
-                                                                              (int2*)ctx->ranges.ptr);
+    ranges_kernel<TileKey><<<grid_for(((int64_t)k + 7) / 8, 256), 256, 0, s>>>((int64_t)k, k_dev, sorted_tiles,
+                                                                              ctx->tiles_x, (int2*)ctx->ranges.ptr);
     return check_launch(ctx, "ranges_kernel");
 }
 
@@ -479,18 +490,28 @@ darbs_status run_binning(darbs_cuda_ctx* ctx, int64_t n, const float* mu2, const
     ctx->cur_order_buf = kDepthPasses & 1;
     const unsigned* order = ctx->cur_order_buf ? or1 : or0;
 
-    // the host waits for K only (published before the depth sort): the GPU still has the sort
-    // queued, so it does not idle while the rest of the iteration is being launched
-    DARBS_CUDA_TRY(ctx, cudaEventSynchronize(ctx->k_ready));
-    const unsigned long long k = *(volatile unsigned long long*)ctx->pinned;
-    if (k >= (1ull << 30)) return fail(ctx, DARBS_INVALID_PARAMETER, "more than 2^30 tile entries");
+    unsigned long long k;
+    const unsigned long long* k_dev = nullptr;
+    if (ctx->entry_capacity > 0 && rects_done) {
+        // the caller vouches for K <= capacity (darbs_cuda_set_entry_capacity): nothing of this view is
+        // read back here, the kernels take K from the device and the host runs on; a view that breaks
+        // the promise is truncated by expand_kernel and reported through the loss slot
+        k = (unsigned long long)ctx->entry_capacity;
+        k_dev = &scalars->total_entries;
+    } else {
+        // the host waits for K only (published before the depth sort): the GPU still has the sort
+        // queued, so it does not idle while the rest of the iteration is being launched
+        DARBS_CUDA_TRY(ctx, cudaEventSynchronize(ctx->k_ready));
+        k = *(volatile unsigned long long*)ctx->pinned;
+        if (k >= (1ull << 30)) return fail(ctx, DARBS_INVALID_PARAMETER, "more than 2^30 tile entries");
+    }
     ctx->fwd_entries = (int64_t)k;
     if (k == 0) return DARBS_OK;
 
     // 2.-4. entries in depth order, stable sort on the tile, ranges
     if (ctx->tiles_x <= 256 && ctx->tiles_y <= 256)
-        return tile_sort<unsigned short>(ctx, n, (int64_t)k, order, rects, touched);
-    return tile_sort<unsigned>(ctx, n, (int64_t)k, order, rects, touched);
+        return tile_sort<unsigned short>(ctx, n, (int64_t)k, k_dev, order, rects, touched);
+    return tile_sort<unsigned>(ctx, n, (int64_t)k, k_dev, order, rects, touched);
 }
 
 darbs_status export_bins(darbs_cuda_ctx* ctx, int64_t n, int32_t* tile_ranges, int32_t* point_list,

@@ -91,6 +91,7 @@ struct darbs_cuda_ctx {
     int64_t launches = 0;
     int exact = 1;
     int timing = 0;
+    int64_t entry_capacity = 0;  // > 0: evaluate_view does not wait for K (darbs_cuda_set_entry_capacity)
     int cull_segment = 0;   // entries of a tile's list the cull kernel covers (0: per family, render.cu cull_segment)
     int deterministic = 0;  // fixed-point accumulation of gradients and loss sums (darbs_cuda_set_deterministic)
     int accumulate = 1;  // evaluate_view adds to param_grads (0: the next call overwrites)
@@ -180,6 +181,7 @@ darbs_status make_kparams(darbs_cuda_ctx* ctx, const darbs_kernel_spec* spec, KP
 // stages run separately).
 static constexpr int kSlotsK = 64;       // K is accumulated over this many addresses, by block index
 static constexpr int kSlotsKBase = 32;   // their position in ctx->counters, in u64 units
+static constexpr int kOverflowAt = 13;   // entry-capacity overflow flag (u64), inside the 40 bytes a loss slot copies
 
 struct SplatSinks {
     float4* recs = nullptr;           // n x kRecVecs

@@ -292,7 +292,8 @@ __device__ __forceinline__ void pass_body(const KeyT* __restrict__ keys_in, cons
 template <typename KeyT, int THREADS, int ITEMS>
 __global__ void __launch_bounds__(THREADS, 1024 / THREADS)
 onesweep_kernel(const KeyT* __restrict__ keys_in, const unsigned* __restrict__ vals_in,
-                KeyT* __restrict__ keys_out, unsigned* __restrict__ vals_out, unsigned n, int shift, int bits,
+                KeyT* __restrict__ keys_out, unsigned* __restrict__ vals_out, unsigned n_bound,
+                const unsigned long long* __restrict__ n_dev, int shift, int bits,
                 const unsigned* __restrict__ ghist, unsigned* __restrict__ status, unsigned* __restrict__ ticket
 #ifdef DARBS_RADIX_PROFILE
                 , long long* __restrict__ prof
@@ -321,6 +322,17 @@ onesweep_kernel(const KeyT* __restrict__ keys_in, const unsigned* __restrict__ v
     __syncthreads();
     const unsigned chunk = s_chunk;
     const unsigned mask = (1u << bits) - 1u;
+    // the element count: the launch's bound, or (n_dev given) the count a kernel left on the device,
+    // clamped to the bound the buffers were sized for; chunks past it have nothing to do
+    unsigned n = n_bound;
+    if (n_dev) {
+        // more elements than the bound: the digit histograms count all of them, so positions would
+        // leave the buffers; the producer has flagged the overflow and the sort is skipped
+        const unsigned long long nd = *n_dev;
+        if (nd > (unsigned long long)n_bound) return;
+        n = (unsigned)nd;
+    }
+    if ((unsigned long long)chunk * kChunk >= n) return;
 #ifdef DARBS_RADIX_PROFILE
 #define RADIX_PROF_ARGS , t_, tn_
 #else
@@ -370,10 +382,12 @@ static long long* g_prof = nullptr;
 #endif
 // All passes of `plan` over n pairs, ping-ponging between (k0, v0) and (k1, v1).  hist: the
 // digit histograms [pass][kBins], complete; tickets[pass] and status[pass][chunk][kBins] zero.
+// n_dev (optional): the true count lives on the device and n is only its bound (buffers, grid).
 // The sorted pairs end in buffer (plan.passes & 1).
 template <typename KeyT>
 inline cudaError_t launch_passes(KeyT* k0, unsigned* v0, KeyT* k1, unsigned* v1, unsigned n, const Plan& plan,
-                                 unsigned* tickets, const unsigned* hist, unsigned* status, cudaStream_t stream) {
+                                 unsigned* tickets, const unsigned* hist, unsigned* status, cudaStream_t stream,
+                                 const unsigned long long* n_dev = nullptr) {
     if (n == 0) return cudaSuccess;
     using Shape = PassShape<KeyT, kPassThreads, kPassItems>;
     auto kernel = onesweep_kernel<KeyT, kPassThreads, kPassItems>;
@@ -387,7 +401,7 @@ inline cudaError_t launch_passes(KeyT* k0, unsigned* v0, KeyT* k1, unsigned* v1,
     for (int p = 0; p < plan.passes; ++p) {
         const bool fwd = (p & 1) == 0;
         kernel<<<chunks, kPassThreads, Shape::kSmem, stream>>>(
-            fwd ? k0 : k1, fwd ? v0 : v1, fwd ? k1 : k0, fwd ? v1 : v0, n, plan.shift[p], plan.bits[p],
+            fwd ? k0 : k1, fwd ? v0 : v1, fwd ? k1 : k0, fwd ? v1 : v0, n, n_dev, plan.shift[p], plan.bits[p],
             hist + (size_t)p * kBins, status + (size_t)p * chunks * kBins, tickets + p
 #ifdef DARBS_RADIX_PROFILE
             , g_prof

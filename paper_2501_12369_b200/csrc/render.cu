@@ -1318,7 +1318,10 @@ int cull_segment(const darbs_cuda_ctx* ctx, const KParams& kp) {
     if (ctx->cull_segment > 0) return ctx->cull_segment;
     const int base = (kp.fam == FAM_HCOS2 || kp.fam == FAM_IMQ) ? 256 : 384;
     const long long tiles = (long long)ctx->tiles_x * ctx->tiles_y;
-    return (tiles > 0 && 2 * ctx->fwd_entries >= 3 * (long long)base * tiles) ? base : kNoSegment;
+    // with a promised capacity instead of K (darbs_cuda_set_entry_capacity) the host only knows the
+    // bound; the promise is documented as 1.25 x the expected K
+    const long long k = ctx->entry_capacity > 0 ? ctx->fwd_entries * 4 / 5 : ctx->fwd_entries;
+    return (tiles > 0 && 2 * k >= 3 * (long long)base * tiles) ? base : kNoSegment;
 }
 
 darbs_status launch_cull(darbs_cuda_ctx* ctx, const KParams& kp) {

@@ -298,3 +298,48 @@ def test_adam_matches_oracle(ctx, port):
     p, m, v = p0.copy(), np.zeros(dim, np.float32), np.zeros(dim, np.float32)
     ctx.adam_step(p, np.zeros(dim, np.float32), m, v, lrs, 1)
     assert np.array_equal(p, p0)
+
+
+def test_entry_capacity_removes_the_wait_and_reports_overflow(darbs):
+    """darbs_cuda_set_entry_capacity: with a capacity >= K the view is bit-identical to the default
+    path (which waits for K); with a capacity below K nothing is written out of bounds, the view
+    renders as if it were empty and the call that collects its loss reports contract_violation."""
+    import torch
+
+    from paper_2501_12369_b200 import synthetic as syn
+
+    name, n, w, h = "raised-cosine", 40000, 320, 240
+    gk, psi = darbs.kernel_preset(name), darbs.default_psi(name)
+    truth = syn.scene_b(n, 1, half_extent=(1.0, 0.7, 0.7), scale_range=(0.004, 0.02))
+    init = syn.perturb(truth, 2)
+    cam = syn.orbit_camera(0, 1, w, h, 300.0)
+    dev = torch.device("cuda", 0)
+    with darbs.Context(0) as ctx:
+        ctx.use_torch_stream()
+        ctx.set_deterministic(True)
+        target = torch.empty((h, w, 3), dtype=torch.float32, device=dev)
+        ctx.evaluate_view(gk, psi, torch.from_numpy(truth).to(dev), cam, (0, 0, 0), grad_image=torch.zeros_like(target),
+                          image_out=target)
+        p = torch.from_numpy(init).to(dev)
+
+        def run():
+            g = torch.zeros((n, 14), device=dev)
+            img = torch.empty_like(target)
+            loss = ctx.evaluate_view(gk, psi, p, cam, (0, 0, 0), target=target, lam=0.2, param_grads=g, image_out=img,
+                                     accumulate=False)
+            return loss, g.cpu().numpy(), img.cpu().numpy()
+
+        loss0, g0, img0 = run()
+        k = ctx.work_counters()["entries"]
+        assert k > 50000
+        ctx.set_entry_capacity(int(1.25 * k))
+        loss1, g1, img1 = run()
+        assert ctx.work_counters()["entries"] == k
+        assert loss1 == loss0 and np.array_equal(g1, g0) and np.array_equal(img1, img0)
+        ctx.set_entry_capacity(k // 2)
+        with pytest.raises(darbs.DarbsError) as e:
+            run()
+        assert e.value.status == 4 and "capacity" in str(e.value)
+        ctx.set_entry_capacity(0)
+        loss2, g2, img2 = run()
+        assert loss2 == loss0 and np.array_equal(g2, g0)
