@@ -65,18 +65,20 @@ def test_bins_properties_at_full_size(ctx, big, name):
     assert np.all(order[1:][ties] > order[:-1][ties])  # index tie-break (rasterizer.cpp:33)
 
 
-@pytest.mark.parametrize("name", ["gaussian", "half-cosine-sq", "raised-cosine", "inv-multiquadratic"])
-def test_kernel_matches_the_oracle_at_full_size(ctx, port, darbs, big, name):
-    """rasterizer.cpp:25-53 (bins), :55-112 (forward), :147-234 (backward) at 1 M splats, 1080p."""
-    s = big(name)
+def compare_with_oracle(ctx, port, darbs, s, name, n, w, h):
+    """rasterizer.cpp:25-53 (bins), :55-112 (forward), :147-234 (backward) on one random_scene."""
     k = port.preset(name)
     gk = darbs.kernel_preset(name)
-    offsets, plist, order = port.bin(s, W, H)
+    offsets, plist, order = port.bin(s, w, h)
     g = scene_f32(s)
-    b = ctx.bin(g["mu2"], g["conic"], g["radius"], g["depth"], W, H)
+    b = ctx.bin(g["mu2"], g["conic"], g["radius"], g["depth"], w, h)
     assert np.array_equal(b["point_list"], plist) and np.array_equal(b["depth_order"], order)
-    ref = port.forward(k, s, W, H, BG, threads=0, keep=True)
-    out = ctx.forward(gk, **g, width=W, height=H, background=BG)
+    nonempty = np.diff(offsets) > 0
+    assert np.array_equal(b["tile_ranges"][nonempty, 0], offsets[:-1][nonempty])
+    assert np.array_equal(b["tile_ranges"][nonempty, 1], offsets[1:][nonempty])
+    del b, plist, order
+    ref = port.forward(k, s, w, h, BG, threads=0, keep=True)
+    out = ctx.forward(gk, **g, width=w, height=h, background=BG)
     wc = ctx.work_counters()
     # bit-exact at full size too: the pixels whose FP32 transmittance comes within the guard band of
     # the floor (wc["tfloor"] of them) are composited again in FP64 by the forward kernel
@@ -85,11 +87,11 @@ def test_kernel_matches_the_oracle_at_full_size(ctx, port, darbs, big, name):
     assert wc["tfloor"] > 0
     assert np.abs(out["image"] - ref["image"]).max() <= IMG_TOL
     assert np.abs(out["t_final"] - ref["t_final"]).max() <= IMG_TOL
-    gi = port.random_image_grad(W, H, 99)
+    gi = port.random_image_grad(w, h, 99)
     st, ref_grads = port.backward(ref["handle"], k, gi, s, threads=0)
     port.forward_free(ref["handle"])
     assert st == 0
-    grads = ctx.backward(gk, f32(gi), N)
+    grads = ctx.backward(gk, f32(gi), n)
     floor = np.maximum(1e-4, 1e-3 * np.abs(ref_grads).max(axis=0, keepdims=True))
     err = rel_err(grads, ref_grads, floor)
     # every splat under a mismatching pixel (tens of contributors, nine components each) may differ;
@@ -97,6 +99,23 @@ def test_kernel_matches_the_oracle_at_full_size(ctx, port, darbs, big, name):
     assert (err > 1e-3).sum() <= 9 * 64 * int(bad.sum()) + 1e-5 * err.size, (err.max(), int((err > 1e-3).sum()))
     assert err.max() <= 2e-2
     assert (rel_err(grads, ref_grads, 1e-4) <= 1e-3).mean() >= 0.999
+    return wc
+
+
+@pytest.mark.parametrize("name", ["gaussian", "half-cosine-sq", "raised-cosine", "inv-multiquadratic"])
+def test_kernel_matches_the_oracle_at_full_size(ctx, port, darbs, big, name):
+    compare_with_oracle(ctx, port, darbs, big(name), name, N, W, H)
+
+
+@pytest.mark.parametrize("name", ["gaussian", "half-cosine-sq", "raised-cosine", "inv-multiquadratic"])
+def test_kernel_matches_the_oracle_at_the_sweep_maximum(ctx, port, darbs, name):
+    """BASELINE.json configs[4]'s largest point, 5,000,000 splats at 3840x2160 (32,400 tiles, more
+    than 2^24 tile entries): the same direct comparison — lists, ranges and depth order bit-exact,
+    processed / contributors bit-exact, image and gradients by the 1 M test's bars."""
+    n, w, h = 5_000_000, 3840, 2160
+    s = port.random_scene(port.preset(name), n, w, h, 3)
+    wc = compare_with_oracle(ctx, port, darbs, s, name, n, w, h)
+    assert wc["entries"] > 1 << 24
 
 
 @pytest.mark.parametrize("name", ["gaussian", "raised-cosine", "inv-multiquadratic"])
