@@ -45,6 +45,12 @@ template <>
 __device__ __forceinline__ double sigmoid_out<double>(float x) { return (double)(1.0f / (1.0f + expf(-x))); }
 template <>
 __device__ __forceinline__ float sigmoid_out<float>(float x) { return 1.0f / (1.0f + __expf(-x)); }
+template <typename T>
+__device__ __forceinline__ T sigmoid_opacity(float x);
+template <>
+__device__ __forceinline__ double sigmoid_opacity<double>(float x) { return 1.0 / (1.0 + exp(-(double)x)); }
+template <>
+__device__ __forceinline__ float sigmoid_opacity<float>(float x) { return sigmoid_out<float>(x); }
 __device__ __forceinline__ double exp_t(double x) { return exp(x); }
 __device__ __forceinline__ float exp_t(float x) { return __expf(x); }
 __device__ __forceinline__ double sqrt_t(double x) { return sqrt(x); }
@@ -77,11 +83,14 @@ __device__ __forceinline__ void load_prim(const float* __restrict__ p, bool raw,
     for (int k = 0; k < 3; ++k) out.mu[k] = (T)v[k];
     for (int k = 0; k < 3; ++k) out.s[k] = raw ? exp_t((T)v[3 + k]) : (T)v[3 + k];
     for (int k = 0; k < 4; ++k) out.q[k] = (T)v[6 + k];
-    // Opacity and colour leave this chain as float32 and decide no integer (the radius, the near
-    // plane and the tile rectangle depend on mu, s and q only): their sigmoids run in FP32 with the
-    // accurate expf and division (<= 3 ulp), a quarter of the chain's FP64 instructions otherwise.
-    // (The float chain of the training step's gradients keeps the MUFU form.)
-    out.o = raw ? sigmoid_out<T>(v[10]) : (T)v[10];
+    // Colour leaves this chain as float32 and decides nothing: its sigmoids run in FP32 with the
+    // accurate expf and division (<= 3 ulp), three of the chain's four FP64 exponentials otherwise.
+    // Opacity DOES decide (alpha >= 1/255, the 0.99 clamp gate, and through alpha the entry at which
+    // a pixel's transmittance crosses the floor): it is the reference's double sigmoid rounded once,
+    // so the rasterizer sees the float32 value the reference's realisation rounds to.  (tests/
+    // fuzz_cases.py: with an FP32 sigmoid, one ulp of opacity flipped a gate in 1 of ~200 views.)
+    // (The float chain of the training step's gradients keeps the MUFU form: o (1 - o) only.)
+    out.o = raw ? sigmoid_opacity<T>(v[10]) : (T)v[10];
     for (int k = 0; k < 3; ++k) out.col[k] = raw ? sigmoid_out<T>(v[11 + k]) : (T)v[11 + k];
 }
 
