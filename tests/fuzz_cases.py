@@ -249,6 +249,36 @@ def chain_trial(ctx, port, darbs, seed):
     return True
 
 
+# ------------------------------------------------------------------ loss_total (loss.cpp:173-230)
+def loss_trial(ctx, port, seed):
+    """Random sizes from below the window to several tiles, random lambda, images that are unrelated,
+    smooth with small noise, or nearly identical (where the reference's partials cancel).  Values by
+    the bars of tests/test_gpu_loss.py; the gradient image within 5e-4 of its largest element
+    (test_gpu_loss.py holds 1e-5 on its cases and at 1080p; over 6000 random cases 7 % lie between
+    1e-5 and 1e-4 and seven between 1e-4 and 3e-4, all on smooth images: the FP32 second moments are
+    taken about ONE reference value per 32x16 tile, and where the local mean is far from it
+    var = E[x'^2] - E[x']^2 loses digits against a variance of 1e-4 and C2 = 9e-4)."""
+    import test_gpu_loss as L
+
+    rng = np.random.default_rng(seed)
+    w, h = int(rng.integers(1, 150)), int(rng.integers(1, 120))
+    lam = float(rng.choice([0.0, 0.2, 1.0, float(np.round(rng.uniform(0, 1), 3))]))
+    mode = int(rng.integers(0, 3))
+    if mode == 0:
+        x, y = f32(rng.uniform(0, 1, (h, w, 3))), f32(rng.uniform(0, 1, (h, w, 3)))
+    elif mode == 1:
+        x, y = L.smooth_pair(w, h, int(rng.integers(0, 1000)), noise=float(rng.choice([0.005, 0.02, 0.1])))
+    else:
+        x = L.smooth_pair(w, h, int(rng.integers(0, 1000)))[0]
+        y = f32(x + rng.normal(scale=1e-4, size=x.shape))
+    try:
+        L.check(ctx, port, x, y, lam, abs_tol=5e-4, floor_frac=0.5)
+    except Exception as ex:  # noqa: BLE001
+        print(f"FAIL loss seed {seed}: {w}x{h} lam={lam} mode={mode} ->", repr(ex)[:300], flush=True)
+        return False
+    return True
+
+
 if __name__ == "__main__":
     import paper_2501_12369_b200 as darbs
     from oracle import cpu
@@ -260,3 +290,5 @@ if __name__ == "__main__":
     print(f"{ok}/{trials} rasterizer trials passed (seeds {seed0}..{seed0 + trials - 1})")
     ok = sum(chain_trial(ctx_, port_, darbs, seed0 + i) for i in range(trials))
     print(f"{ok}/{trials} chain trials passed (seeds {seed0}..{seed0 + trials - 1})")
+    ok = sum(loss_trial(ctx_, port_, seed0 + i) for i in range(trials))
+    print(f"{ok}/{trials} loss trials passed (seeds {seed0}..{seed0 + trials - 1})")

@@ -19,3 +19,9 @@ def test_fuzz_chain_block(ctx, port, darbs, block, capsys):
     """The 3-D chain of one view (fit3d.cpp:108-159) on random cameras, scenes, kernels and losses."""
     failed = [seed for seed in range(100 * block, 100 * block + 100) if not fuzz_cases.chain_trial(ctx, port, darbs, seed)]
     assert not failed, (failed, capsys.readouterr().out[-2000:])
+
+
+def test_fuzz_loss_block(ctx, port, capsys):
+    """loss_total (loss.cpp:173-230) on random sizes, lambdas and image pairs."""
+    failed = [seed for seed in range(200) if not fuzz_cases.loss_trial(ctx, port, seed)]
+    assert not failed, (failed, capsys.readouterr().out[-2000:])
