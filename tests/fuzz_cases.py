@@ -91,6 +91,14 @@ def trial(ctx, port, seed):
     log = [f"seed {seed}: {name} {w}x{h} n={n}"]
     mutate(rng, s, w, h, log)
     bg = tuple(float(x) for x in f32(rng.uniform(0, 1, 3)))
+    # the two knobs results must not depend on (beyond the stated bars): how much of a tile's list the
+    # cull kernel covers before the forward's blocks cull on by themselves, and the fixed-point
+    # accumulation of the deterministic mode
+    seg = int(rng.choice([0, 0, 1, 7, 16, 33, 64, 200]))
+    det = bool(rng.uniform() < 0.25)
+    log.append(f"segment {seg}, deterministic {det}")
+    ctx.set_cull_segment(seg)
+    ctx.set_deterministic(det)
     try:
         T.check_bins(ctx, port, s, w, h)
         fr = port.forward(k, s, w, h, bg, threads=0, keep=True)
@@ -117,6 +125,9 @@ def trial(ctx, port, seed):
         if os.environ.get("FUZZ_TRACE"):
             traceback.print_exc()
         return False
+    finally:
+        ctx.set_cull_segment(0)
+        ctx.set_deterministic(False)
     return True
 
 
