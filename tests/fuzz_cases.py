@@ -290,6 +290,45 @@ def loss_trial(ctx, port, seed):
     return True
 
 
+# ------------------------------------------------------------------ bin_splats alone, large shapes
+def bins_trial(ctx, port, seed):
+    """rasterizer.cpp:25-53 on shapes the rasterizer trials do not reach: up to 6000 pixels a side (more
+    than 256 tile columns or rows: 32-bit tile keys and a second byte per coordinate), one-tile-wide
+    strips, up to 200 k splats, radii from 0 to thousands of pixels (K up to tens of millions)."""
+    rng = np.random.default_rng(seed)
+    shape = int(rng.integers(0, 4))
+    if shape == 0:
+        w, h = int(rng.integers(1, 6000)), int(rng.integers(1, 6000))
+    elif shape == 1:
+        w, h = int(rng.integers(1, 17)), int(rng.integers(1, 6000))
+    elif shape == 2:
+        w, h = int(rng.integers(1, 6000)), int(rng.integers(1, 17))
+    else:
+        w, h = int(rng.integers(1, 700)), int(rng.integers(1, 700))
+    n = int(np.exp(rng.uniform(0, np.log(200_000))))
+    k = port.preset(str(rng.choice(["gaussian", "raised-cosine"])))
+    s = port.random_scene(k, n, w, h, int(rng.integers(0, 1000)))
+    tiles = ((w + 15) // 16) * ((h + 15) // 16)
+    # radii: keep K below ~3e7 (a splat of radius R touches about (2R/16 + 1)^2 tiles)
+    rmax = 16.0 * max(1.0, np.sqrt(min(3e7 / n, tiles)) / 2.0)
+    mode = int(rng.integers(0, 3))
+    if mode == 1:
+        s.radius[:] = np.floor(rng.uniform(0, rmax, n))
+    elif mode == 2:
+        s.radius[:] = np.floor(np.exp(rng.uniform(0, np.log(rmax + 1.0), n)))
+        s.radius[rng.integers(0, n, 3)] = 10_000.0
+    if rng.uniform() < 0.3:
+        s.depth[:] = f32(rng.choice(s.depth[: max(1, n // 50)], n))
+    if rng.uniform() < 0.2:
+        s.radius[rng.integers(0, n, max(1, n // 100))] = np.nan
+    try:
+        T.check_bins(ctx, port, s, w, h)
+    except Exception as ex:  # noqa: BLE001
+        print(f"FAIL bins seed {seed}: {w}x{h} n={n} mode={mode} ->", repr(ex)[:300], flush=True)
+        return False
+    return True
+
+
 if __name__ == "__main__":
     import paper_2501_12369_b200 as darbs
     from oracle import cpu
@@ -301,5 +340,7 @@ if __name__ == "__main__":
     print(f"{ok}/{trials} rasterizer trials passed (seeds {seed0}..{seed0 + trials - 1})")
     ok = sum(chain_trial(ctx_, port_, darbs, seed0 + i) for i in range(trials))
     print(f"{ok}/{trials} chain trials passed (seeds {seed0}..{seed0 + trials - 1})")
+    ok = sum(bins_trial(ctx_, port_, seed0 + i) for i in range(max(1, trials // 20)))
+    print(f"{ok}/{max(1, trials // 20)} large-shape binning trials passed")
     ok = sum(loss_trial(ctx_, port_, seed0 + i) for i in range(trials))
     print(f"{ok}/{trials} loss trials passed (seeds {seed0}..{seed0 + trials - 1})")

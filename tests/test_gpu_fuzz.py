@@ -25,3 +25,9 @@ def test_fuzz_loss_block(ctx, port, capsys):
     """loss_total (loss.cpp:173-230) on random sizes, lambdas and image pairs."""
     failed = [seed for seed in range(200) if not fuzz_cases.loss_trial(ctx, port, seed)]
     assert not failed, (failed, capsys.readouterr().out[-2000:])
+
+
+def test_fuzz_bins_block(ctx, port, capsys):
+    """bin_splats on large and degenerate tile grids (32-bit tile keys, strips, K in the millions)."""
+    failed = [seed for seed in range(40) if not fuzz_cases.bins_trial(ctx, port, seed)]
+    assert not failed, (failed, capsys.readouterr().out[-2000:])
