@@ -47,13 +47,29 @@ namespace darbs_b200 {
 namespace {
 
 constexpr int kWin = 11, kHalf = 5;
-constexpr int kTW = 32, kTH = 16;              // tile, pixels
+#ifndef DARBS_LOSS_TH
+#define DARBS_LOSS_TH 16
+#endif
+#ifndef DARBS_LOSS_PX
+#define DARBS_LOSS_PX 4
+#endif
+#ifndef DARBS_LOSS_MINB
+#define DARBS_LOSS_MINB 5
+#endif
+#ifndef DARBS_LOSS_AHEAD
+#define DARBS_LOSS_AHEAD 4
+#endif
+constexpr int kTW = 32, kTH = DARBS_LOSS_TH;   // tile, pixels
 constexpr int kCols = 3 * (kTW + 2 * kHalf);   // 126 float columns with halo
-constexpr int kRowsIn = kTH + 2 * kHalf;       // 26 input rows
-constexpr int kOut = 12;                       // floats per phase-2 thread: 4 pixels x 3 channels
-constexpr int kSpan = kOut + 3 * (kWin - 1);   // 42 floats feed them
+constexpr int kRowsIn = kTH + 2 * kHalf;       // input rows
+constexpr int kPX = DARBS_LOSS_PX;             // pixels per phase-2 thread
+constexpr int kGroups = kTW / kPX;             // phase-2 threads per tile row
+constexpr int kOut = 3 * kPX;                  // floats per phase-2 thread: kPX pixels x 3 channels
+constexpr int kSpan = kOut + 3 * (kWin - 1);   // floats that feed them
 constexpr int kLossThreads = 128;
-static_assert(kLossThreads >= kCols && kLossThreads == kTH * (kTW / 4), "thread mapping");
+constexpr int kAhead = DARBS_LOSS_AHEAD;        // rows of global loads in flight per thread in the column passes
+static_assert(kLossThreads >= kCols && kLossThreads == kTH * kGroups, "thread mapping");
+static_assert(kPX == 4 || kPX == 2, "vector width of the row accesses");
 
 struct Window {
     float k[kWin];
@@ -108,10 +124,11 @@ __device__ __forceinline__ void block_sum3(float a, float b, float c, double* __
     }
 }
 
-// 12 consecutive floats of a row, as three 128-bit accesses when the row is 16-byte aligned
+// kOut consecutive floats of a row, as three 128-bit (kPX = 4) or 64-bit (kPX = 2) accesses when
+// the row is 16-byte aligned
 template <bool VEC>
 __device__ __forceinline__ void load12(const float* __restrict__ p, int valid, float out[kOut]) {
-    if constexpr (VEC) {
+    if constexpr (VEC && kPX == 4) {
 #pragma unroll
         for (int q = 0; q < 3; ++q) {
             const float4 v = __ldg(reinterpret_cast<const float4*>(p) + q);
@@ -119,6 +136,13 @@ __device__ __forceinline__ void load12(const float* __restrict__ p, int valid, f
             out[4 * q + 1] = v.y;
             out[4 * q + 2] = v.z;
             out[4 * q + 3] = v.w;
+        }
+    } else if constexpr (VEC) {
+#pragma unroll
+        for (int q = 0; q < kOut / 2; ++q) {
+            const float2 v = __ldg(reinterpret_cast<const float2*>(p) + q);
+            out[2 * q + 0] = v.x;
+            out[2 * q + 1] = v.y;
         }
     } else {
 #pragma unroll
@@ -128,10 +152,13 @@ __device__ __forceinline__ void load12(const float* __restrict__ p, int valid, f
 
 template <bool VEC>
 __device__ __forceinline__ void store12(float* __restrict__ p, int valid, const float v[kOut]) {
-    if constexpr (VEC) {
+    if constexpr (VEC && kPX == 4) {
 #pragma unroll
         for (int q = 0; q < 3; ++q)
             reinterpret_cast<float4*>(p)[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+    } else if constexpr (VEC) {
+#pragma unroll
+        for (int q = 0; q < kOut / 2; ++q) reinterpret_cast<float2*>(p)[q] = make_float2(v[2 * q], v[2 * q + 1]);
     } else {
 #pragma unroll
         for (int e = 0; e < kOut; ++e)
@@ -141,7 +168,7 @@ __device__ __forceinline__ void store12(float* __restrict__ p, int valid, const 
 
 // ---------------------------------------------------------------- moments + SSIM partials
 template <bool VEC>
-__global__ void __launch_bounds__(kLossThreads, 5)
+__global__ void __launch_bounds__(kLossThreads, DARBS_LOSS_MINB)
 ssim_map_kernel(Window win, int w, int h, const float* __restrict__ image,
                 const float* __restrict__ target, float scale, int want_maps,
                 float* __restrict__ fa, float* __restrict__ fe, float* __restrict__ fd,
@@ -175,11 +202,22 @@ ssim_map_kernel(Window win, int w, int h, const float* __restrict__ image,
             a01[o] = a23[o] = make_float2(0.f, 0.f);
             a4[o] = 0.f;
         }
+        // the rows are requested kAhead iterations before their use: a warp's walk down its columns
+        // is otherwise one dependent global load per row (measured: the kernel's long-scoreboard stalls)
+        float xq[kAhead], tq[kAhead];
+#pragma unroll
+        for (int i = 0; i < kAhead && i < kRowsIn; ++i) {
+            xq[i] = __ldg(ip + s_row[i]);
+            tq[i] = __ldg(tp + s_row[i]);
+        }
 #pragma unroll
         for (int i = 0; i < kRowsIn; ++i) {
-            const int off = s_row[i];
-            const float xv = __ldg(ip + off);
-            const float xs = xv - refx, ds = (xv - __ldg(tp + off)) - refd;
+            const float xv = xq[i % kAhead], tv = tq[i % kAhead];
+            if (i + kAhead < kRowsIn) {
+                xq[i % kAhead] = __ldg(ip + s_row[i + kAhead]);
+                tq[i % kAhead] = __ldg(tp + s_row[i + kAhead]);
+            }
+            const float xs = xv - refx, ds = (xv - tv) - refd;
             const float2 p01 = make_float2(xs, ds), p23 = make_float2(xs * xs, ds * ds);
             const float p4 = xs * ds;
 #pragma unroll
@@ -201,8 +239,8 @@ ssim_map_kernel(Window win, int w, int h, const float* __restrict__ image,
     }
     __syncthreads();
     // ---- phase 2: rows (filter_x, loss.cpp:47-60) and ssim_terms (loss.cpp:124-140)
-    const int o = tid >> 3, g = tid & 7;
-    const int gy = y0 + o, gx0 = x0 + 4 * g;
+    const int o = tid / kGroups, g = tid % kGroups;
+    const int gy = y0 + o, gx0 = x0 + kPX * g;
     float sum_abs = 0.f, sum_sq = 0.f, sum_dssim = 0.f;
     if (gy < h && gx0 < w) {
         float2 r01[kOut], r23[kOut];
@@ -246,7 +284,7 @@ ssim_map_kernel(Window win, int w, int h, const float* __restrict__ image,
                 r4[e] = acc;
             }
         }
-        const int valid = 3 * min(4, w - gx0);
+        const int valid = 3 * min(kPX, w - gx0);
         const size_t p = ((size_t)gy * w + gx0) * 3;
         float xc[kOut], yc[kOut];
         load12<VEC>(image + p, valid, xc);
@@ -319,13 +357,22 @@ __device__ __forceinline__ void grad_interior_tile(const Window& win, int w, int
             a01[o] = make_float2(0.f, 0.f);
             a2[o] = 0.f;
         }
-#pragma unroll
-        for (int i = 0; i < kRowsIn; ++i) {
+        float aq[kAhead], eq[kAhead], dq[kAhead];  // rows requested kAhead iterations ahead, as in ssim_map_kernel
+        auto fetch = [&](int i, float& a, float& e, float& d) {
             const int roff = s_row[i];
             const bool in = col_in && roff >= 0;
             const int p = in ? roff + cbase : 0;
-            const float2 p01 = in ? make_float2(__ldg(fa + p), __ldg(fe + p)) : make_float2(0.f, 0.f);
-            const float p2 = in ? __ldg(fd + p) : 0.f;
+            a = in ? __ldg(fa + p) : 0.f;
+            e = in ? __ldg(fe + p) : 0.f;
+            d = in ? __ldg(fd + p) : 0.f;
+        };
+#pragma unroll
+        for (int i = 0; i < kAhead && i < kRowsIn; ++i) fetch(i, aq[i], eq[i], dq[i]);
+#pragma unroll
+        for (int i = 0; i < kRowsIn; ++i) {
+            const float2 p01 = make_float2(aq[i % kAhead], eq[i % kAhead]);
+            const float p2 = dq[i % kAhead];
+            if (i + kAhead < kRowsIn) fetch(i + kAhead, aq[i % kAhead], eq[i % kAhead], dq[i % kAhead]);
 #pragma unroll
             for (int o = 0; o < kTH; ++o) {
                 const int t = i - o;
@@ -343,9 +390,9 @@ __device__ __forceinline__ void grad_interior_tile(const Window& win, int w, int
     }
     __syncthreads();
     // ---- phase 2: rows (scatter_x, loss.cpp:76-89) and the combination (loss.cpp:186, :222-224)
-    const int o = tid >> 3, g = tid & 7;
-    const int gy = y0 + o, gx0 = x0 + 4 * g;
-    if (gy < kHalf || gy >= h - kHalf || gx0 >= w - kHalf || gx0 + 3 < kHalf) return;  // border kernel's
+    const int o = tid / kGroups, g = tid % kGroups;
+    const int gy = y0 + o, gx0 = x0 + kPX * g;
+    if (gy < kHalf || gy >= h - kHalf || gx0 >= w - kHalf || gx0 + kPX - 1 < kHalf) return;  // border kernel's
     float2 r01[kOut];
     float r2[kOut];
     {
@@ -374,7 +421,7 @@ __device__ __forceinline__ void grad_interior_tile(const Window& win, int w, int
             r2[e] = acc;
         }
     }
-    const int valid = 3 * min(4, w - gx0);
+    const int valid = 3 * min(kPX, w - gx0);
     const size_t p = ((size_t)gy * w + gx0) * 3;
     float xc[kOut], yc[kOut], out[kOut];
     load12<VEC>(image + p, valid, xc);
@@ -385,7 +432,7 @@ __device__ __forceinline__ void grad_interior_tile(const Window& win, int w, int
         out[e] = coef_l1 * (float)((d > 0.f) - (d < 0.f)) + r01[e].x + xc[e] * r01[e].y - d * r2[e];
     }
     // the group may straddle the five-pixel band on the left or right
-    const bool whole = gx0 >= kHalf && gx0 + 3 < w - kHalf;
+    const bool whole = gx0 >= kHalf && gx0 + kPX - 1 < w - kHalf;
     if (whole) {
         store12<VEC>(grad + p, valid, out);
     } else {
