@@ -101,7 +101,9 @@ DARBS_API void darbs_cuda_destroy(darbs_cuda_ctx* ctx);
 DARBS_API const char* darbs_cuda_last_error(const darbs_cuda_ctx* ctx);
 /* Use an externally owned cudaStream_t (e.g. torch's current stream) for all
  * subsequent work; NULL restores the context's own stream.  To run on the legacy
- * default stream pass cudaStreamLegacy ((void*)1), not NULL. */
+ * default stream pass cudaStreamLegacy ((void*)1), not NULL.  Switching drains the stream that is
+ * left; binding the stream the context already runs on is free (and legal while that stream is
+ * capturing a CUDA graph). */
 DARBS_API darbs_status darbs_cuda_set_stream(darbs_cuda_ctx* ctx, void* cuda_stream);
 DARBS_API darbs_status darbs_cuda_synchronize(darbs_cuda_ctx* ctx);
 /* Number of kernels this library has launched on the context since creation
@@ -123,7 +125,12 @@ DARBS_API darbs_status darbs_cuda_set_deterministic(darbs_cuda_ctx* ctx, int ena
  * training loop whose previous iterations saw K_prev can pass 1.25 K_prev — sets it here
  * (entries > 0) and the wait disappears: buffers and grids are sized by the capacity, the kernels
  * take K from the device, and an iteration can be queued without any host synchronisation
- * (CUDA-graph capturable).  A view with K > capacity is TRUNCATED safely (no write leaves the
+ * (CUDA-graph capturable: darbs_cuda_evaluate_view with DARBS_DEVICE arrays on a capturing stream
+ * records the whole view; such a view reports neither loss nor status - loss_out must be NULL and
+ * nothing is queued for darbs_cuda_pop_loss - so check K <= capacity with an eager view now and
+ * then; darbs_cuda_adam_step takes its bias correction by value and is launched outside the graph;
+ * tests/test_gpu_geometry.py::test_a_view_is_capturable_in_a_cuda_graph, bench.py's device-resident
+ * arm).  A view with K > capacity is TRUNCATED safely (no write leaves the
  * buffers) and reported as DARBS_CONTRACT_VIOLATION by the call that collects its loss
  * (darbs_cuda_pop_loss, or evaluate_view / train_step with loss_out).  0 restores the wait.
  * Heuristics that look at K (the cull segment) take the capacity to be 1.25 x the expected K.

@@ -410,8 +410,12 @@ const char* darbs_cuda_last_error(const darbs_cuda_ctx* ctx) {
 darbs_status darbs_cuda_set_stream(darbs_cuda_ctx* ctx, void* cuda_stream) {
     CTX_OR_FAIL(ctx);
     DeviceGuard guard(ctx->device);
+    cudaStream_t next = cuda_stream ? (cudaStream_t)cuda_stream : ctx->own_stream;
+    // binding the stream the context already runs on is free (callers re-bind before every call
+    // when they share the stream with other libraries; it may also be capturing a graph)
+    if (next == ctx->stream) return DARBS_OK;
     DARBS_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
-    ctx->stream = cuda_stream ? (cudaStream_t)cuda_stream : ctx->own_stream;
+    ctx->stream = next;
     return DARBS_OK;
 }
 
@@ -873,6 +877,17 @@ darbs_status darbs_cuda_evaluate_view(darbs_cuda_ctx* ctx, const darbs_kernel_sp
     // flags (2 ints) and loss sums (3 doubles) travel to a pinned ring slot; the caller either waits
     // for them now (loss_out) or collects them later with darbs_cuda_pop_loss, so that a training
     // loop never has to drain the stream between two iterations
+    // A view that is being captured into a CUDA graph (possible with darbs_cuda_set_entry_capacity:
+    // nothing above synchronises with the host) reports neither loss nor status: the ring's events
+    // cannot be waited for from inside a capture, and a replay has no call to return them from.
+    {
+        cudaStreamCaptureStatus capturing = cudaStreamCaptureStatusNone;
+        DARBS_CUDA_TRY(ctx, cudaStreamIsCapturing(ctx->stream, &capturing));
+        if (capturing != cudaStreamCaptureStatusNone) {
+            if (loss_out) return fail(ctx, DARBS_CONTRACT_VIOLATION, "evaluate_view: loss_out inside a stream capture");
+            return DARBS_OK;
+        }
+    }
     if (ctx->loss_pending == kLossRing) {  // nobody collects them: forget the oldest
         ctx->loss_head = (ctx->loss_head + 1) % kLossRing;
         --ctx->loss_pending;

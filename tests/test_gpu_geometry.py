@@ -343,3 +343,51 @@ def test_entry_capacity_removes_the_wait_and_reports_overflow(darbs):
         ctx.set_entry_capacity(0)
         loss2, g2, img2 = run()
         assert loss2 == loss0 and np.array_equal(g2, g0)
+
+
+def test_a_view_is_capturable_in_a_cuda_graph(darbs):
+    """With an entry capacity nothing in darbs_cuda_evaluate_view synchronises with the host, so the
+    whole view (preprocess ... parameter gradients) can be captured into
+    a CUDA graph on the caller's stream and replayed: in the deterministic mode every replay is
+    bit-identical to the eager call.  (A captured view reports neither loss nor status.)"""
+    import torch
+
+    from paper_2501_12369_b200 import synthetic as syn
+
+    name, n, w, h = "half-cosine-sq", 30000, 256, 192
+    gk, psi = darbs.kernel_preset(name), darbs.default_psi(name)
+    truth = syn.scene_b(n, 1, half_extent=(1.0, 0.7, 0.7), scale_range=(0.004, 0.02))
+    init = syn.perturb(truth, 2)
+    cam = syn.orbit_camera(0, 1, w, h, 250.0)
+    dev = torch.device("cuda", 0)
+    stream = torch.cuda.Stream(dev)
+    with torch.cuda.stream(stream), darbs.Context(0) as ctx:
+        ctx.use_torch_stream()
+        ctx.set_deterministic(True)
+        target = torch.empty((h, w, 3), dtype=torch.float32, device=dev)
+        ctx.evaluate_view(gk, psi, torch.from_numpy(truth).to(dev), cam, (0, 0, 0), grad_image=torch.zeros_like(target),
+                          image_out=target)
+        p = torch.from_numpy(init).to(dev)
+        g = torch.zeros((n, 14), device=dev)
+        img = torch.empty_like(target)
+
+        def view(want_loss):
+            return ctx.evaluate_view(gk, psi, p, cam, (0, 0, 0), target=target, lam=0.2, param_grads=g, image_out=img,
+                                     accumulate=False, want_loss=want_loss)
+
+        loss0 = view(True)
+        g0, img0 = g.clone(), img.clone()
+        ctx.set_entry_capacity(int(1.25 * ctx.work_counters()["entries"]))
+        view(True)  # buffers sized by the capacity before the capture
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph, stream=stream):
+            ctx.use_torch_stream()
+            view(False)
+        for _ in range(3):
+            g.zero_()
+            img.zero_()
+            graph.replay()
+            stream.synchronize()
+            assert torch.equal(g, g0) and torch.equal(img, img0)
+        ctx.set_entry_capacity(0)
+        assert view(True) == loss0
