@@ -265,7 +265,10 @@ darbs_status forward_device(darbs_cuda_ctx* ctx, const KParams& kp, int64_t n, c
     const size_t px = (size_t)width * height;
     {
         StageScope ts(ctx, ST_BINNING);
-        DARBS_TRY(run_binning(ctx, n, mu2, conic, radius, depth, valid, width, height, preprocessed));
+        ctx->tile_order_wanted = ctx->tile_order_lpt != 0;  // a forward follows: its CTAs take the long tiles first
+        const darbs_status st_bin = run_binning(ctx, n, mu2, conic, radius, depth, valid, width, height, preprocessed);
+        ctx->tile_order_wanted = false;
+        DARBS_TRY(st_bin);
     }
     {
         StageScope ts(ctx, ST_CULL);
@@ -332,6 +335,7 @@ darbs_status darbs_cuda_create(int device, darbs_cuda_ctx** out_ctx) {
     if (!ctx) return fail(nullptr, DARBS_CUDA_ERROR, "out of host memory");
     ctx->device = device;
     ctx->sm_count = prop.multiProcessorCount;
+    if (const char* e = getenv("DARBS_TILE_ORDER")) ctx->tile_order_lpt = atoi(e);
     DeviceGuard guard(device);
     e = cudaStreamCreateWithFlags(&ctx->own_stream, cudaStreamNonBlocking);
     if (e != cudaSuccess) {
@@ -340,6 +344,9 @@ darbs_status darbs_cuda_create(int device, darbs_cuda_ctx** out_ctx) {
     }
     ctx->stream = ctx->own_stream;
     cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking);
+    cudaStreamCreateWithFlags(&ctx->aux_stream, cudaStreamNonBlocking);
+    cudaEventCreateWithFlags(&ctx->ranges_ready, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&ctx->order_ready, cudaEventDisableTiming);
     cudaEventCreateWithFlags(&ctx->copy_begin, cudaEventDisableTiming);
     cudaEventCreateWithFlags(&ctx->copy_done, cudaEventDisableTiming);
     for (int i = 0; i < 16; ++i) cudaEventCreate(&ctx->timer.ev[i]);
@@ -373,7 +380,7 @@ void darbs_cuda_destroy(darbs_cuda_ctx* ctx) {
     cudaStreamSynchronize(ctx->stream);
     destroy_comm(ctx);
     DeviceBuffer* bufs[] = {&ctx->recs, &ctx->rects, &ctx->depth_keys, &ctx->order,
-                            &ctx->tile_keys, &ctx->tile_vals, &ctx->ranges, &ctx->streams, &ctx->stream_count, &ctx->sort_ws, &ctx->tile_status,
+                            &ctx->tile_keys, &ctx->tile_vals, &ctx->ranges, &ctx->streams, &ctx->stream_count, &ctx->sort_ws, &ctx->tile_status, &ctx->tile_order,
                             &ctx->counters, &ctx->t_final, &ctx->processed, &ctx->contributors,
                             &ctx->image, &ctx->valid, &ctx->splat_grads, &ctx->splat_grads_fx, &ctx->grad_image, &ctx->loss_maps};
     for (DeviceBuffer* b : bufs)
@@ -399,6 +406,9 @@ void darbs_cuda_destroy(darbs_cuda_ctx* ctx) {
     if (ctx->copy_begin) cudaEventDestroy(ctx->copy_begin);
     if (ctx->copy_done) cudaEventDestroy(ctx->copy_done);
     if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
+    if (ctx->aux_stream) cudaStreamDestroy(ctx->aux_stream);
+    if (ctx->ranges_ready) cudaEventDestroy(ctx->ranges_ready);
+    if (ctx->order_ready) cudaEventDestroy(ctx->order_ready);
     if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
     delete ctx;
 }

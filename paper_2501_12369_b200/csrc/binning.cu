@@ -360,6 +360,64 @@ radix::Plan tile_plan(int tiles_x, int tiles_y) {
     return plan;
 }
 
+// The render kernels' CTAs take the tiles longest list first: a tile's work grows with its list, the
+// hardware hands CTAs out in index order, and with the long ones started first the launch's tail is
+// made of short ones (raster order leaves whatever the bottom rows of the image hold for last).
+// One CTA: counting sort of the tiles by list length in buckets of 16 entries (order inside a
+// bucket is whatever the atomics give: it only decides when a tile runs, never what it computes).
+constexpr int kOrderBuckets = 512;
+constexpr int kOrderThreads = 1024, kOrderRegs = 8;  // up to 8192 tiles keep their lengths in registers
+__device__ __forceinline__ int order_bucket(int len) { return min(kOrderBuckets - 1, len >> 4); }
+__global__ void __launch_bounds__(kOrderThreads) tile_order_kernel(const int2* __restrict__ ranges, int tiles,
+                                                                   int* __restrict__ order) {
+    __shared__ int cursor[kOrderBuckets];
+    for (int b = threadIdx.x; b < kOrderBuckets; b += kOrderThreads) cursor[b] = 0;
+    int len[kOrderRegs];
+#pragma unroll
+    for (int i = 0; i < kOrderRegs; ++i) {  // independent loads, all in flight at once
+        const int t = threadIdx.x + i * kOrderThreads;
+        len[i] = -1;
+        if (t < tiles) {
+            const int2 r = ranges[t];
+            len[i] = r.y - r.x;
+        }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < kOrderRegs; ++i)
+        if (len[i] >= 0) atomicAdd(&cursor[order_bucket(len[i])], 1);
+    for (int t = threadIdx.x + kOrderRegs * kOrderThreads; t < tiles; t += kOrderThreads) {
+        const int2 r = ranges[t];
+        atomicAdd(&cursor[order_bucket(r.y - r.x)], 1);
+    }
+    __syncthreads();
+    if (threadIdx.x < 32) {  // exclusive scan from the longest bucket down: 16 buckets per lane
+        constexpr int kPer = kOrderBuckets / 32;
+        const int top = kOrderBuckets - 1 - (int)threadIdx.x * kPer;  // this lane's longest bucket
+        int sum = 0;
+        for (int i = 0; i < kPer; ++i) sum += cursor[top - i];
+        int incl = sum;
+        for (int d = 1; d < 32; d <<= 1) {
+            const int v = __shfl_up_sync(0xffffffffu, incl, d);
+            if ((int)threadIdx.x >= d) incl += v;
+        }
+        int run = incl - sum;
+        for (int i = 0; i < kPer; ++i) {
+            const int c = cursor[top - i];
+            cursor[top - i] = run;
+            run += c;
+        }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < kOrderRegs; ++i)
+        if (len[i] >= 0) order[atomicAdd(&cursor[order_bucket(len[i])], 1)] = threadIdx.x + i * kOrderThreads;
+    for (int t = threadIdx.x + kOrderRegs * kOrderThreads; t < tiles; t += kOrderThreads) {
+        const int2 r = ranges[t];
+        order[atomicAdd(&cursor[order_bucket(r.y - r.x)], 1)] = t;
+    }
+}
+
 // Steps 2-4 of the header.  The small part of the sort workspace (tickets, histograms, the
 // expand kernel's status words) was cleared by binning_begin; the status words of the tile passes
 // depend on K and are cleared here.
@@ -400,7 +458,21 @@ darbs_status tile_sort(darbs_cuda_ctx* ctx, int64_t n, int64_t k, const unsigned
     const TileKey* sorted_tiles = ctx->cur_key_buf ? tk1 : tk0;
     ranges_kernel<TileKey><<<grid_for(((int64_t)k + 7) / 8, 256), 256, 0, s>>>((int64_t)k, k_dev, sorted_tiles,
                                                                               ctx->tiles_x, (int2*)ctx->ranges.ptr);
-    return check_launch(ctx, "ranges_kernel");
+    DARBS_TRY(check_launch(ctx, "ranges_kernel"));
+    if (ctx->tile_order_wanted) {
+        // on a second stream, under the cull kernel (which takes the tiles in raster order: neighbours
+        // share records); the forward's launch waits for it (render.cu join_tile_order)
+        const int tiles = ctx->tiles_x * ctx->tiles_y;
+        DARBS_CUDA_TRY(ctx, cudaEventRecord(ctx->ranges_ready, s));
+        DARBS_CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->aux_stream, ctx->ranges_ready, 0));
+        tile_order_kernel<<<1, kOrderThreads, 0, ctx->aux_stream>>>((const int2*)ctx->ranges.ptr, tiles,
+                                                                   (int*)ctx->tile_order.ptr);
+        DARBS_TRY(check_launch(ctx, "tile_order_kernel"));
+        DARBS_CUDA_TRY(ctx, cudaEventRecord(ctx->order_ready, ctx->aux_stream));
+        ctx->tile_order_valid = true;
+        ctx->tile_order_pending = true;
+    }
+    return DARBS_OK;
 }
 
 // Sizes the per-splat buffers of the stage, clears its counters and the tile ranges, and tells
@@ -416,6 +488,8 @@ darbs_status binning_begin(darbs_cuda_ctx* ctx, int64_t n, int width, int height
     if (n >= (int64_t)1 << 30) return fail(ctx, DARBS_INVALID_PARAMETER, "too many splats (2^30 or more)");
 
     DARBS_TRY(reserve(ctx, ctx->ranges, sizeof(int2) * (size_t)(tiles > 0 ? tiles : 1)));
+    DARBS_TRY(reserve(ctx, ctx->tile_order, sizeof(int) * (size_t)(tiles > 0 ? tiles : 1)));
+    ctx->tile_order_valid = false;  // until this view's tile sort has ordered its tiles
     DARBS_CUDA_TRY(ctx, cudaMemsetAsync(ctx->ranges.ptr, 0, sizeof(int2) * (size_t)tiles, s));
     Scalars* scalars = (Scalars*)((unsigned long long*)ctx->counters.ptr + 8);
     // work counters, scalars and the K slots in one clear (what lies between them is scratch)

@@ -86,6 +86,10 @@ struct darbs_cuda_ctx {
     // host -> device uploads that a call does not need until late (the target image of
     // evaluate_view) run on their own stream, fenced by these two events
     cudaStream_t copy_stream = nullptr;
+    cudaStream_t aux_stream = nullptr;                       // the tile ordering runs here, under the cull kernel
+    cudaEvent_t ranges_ready = nullptr, order_ready = nullptr;
+    bool tile_order_pending = false;                         // the stream has not yet waited for order_ready
+    bool tile_order_wanted = false;                          // a forward follows this binning
     cudaEvent_t copy_begin = nullptr, copy_done = nullptr;
     std::string last_error;
     int64_t launches = 0;
@@ -109,6 +113,9 @@ struct darbs_cuda_ctx {
     darbs_b200::DeviceBuffer stream_count; // 2 x 8 tiles int: entries per stream | entries the forward composited
     darbs_b200::DeviceBuffer sort_ws;      // tickets, digit histograms and status words of the sorts (binning.cu)
     darbs_b200::DeviceBuffer tile_status;  // status words of the tile sort's passes (sized by K)
+    darbs_b200::DeviceBuffer tile_order;   // tiles int: tile indices, longest list first (the render kernels' CTA order)
+    bool tile_order_valid = false;         // set by the tile sort of the current forward
+    int tile_order_lpt = 1;                // 0: CTAs take the tiles in raster order
     darbs_b200::DeviceBuffer counters;     // Counters + scalars
     darbs_b200::DeviceBuffer t_final, processed, contributors, image;  // per-pixel aux
     darbs_b200::DeviceBuffer stage_in[8];  // staging for DARBS_HOST calls / internal SoA

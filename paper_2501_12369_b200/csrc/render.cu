@@ -327,10 +327,12 @@ __device__ __forceinline__ bool block_survives(float A, float B, float C, float 
 __global__ void __launch_bounds__(kThreads)
 cull_kernel(KParams kp, const float4* __restrict__ recs, const int2* __restrict__ ranges,
             const int* __restrict__ point_list, int tiles_x, int seg, float4* __restrict__ streams,
-            int* __restrict__ stream_count, unsigned long long* __restrict__ counters) {
+            int* __restrict__ stream_count, unsigned long long* __restrict__ counters,
+            const int* __restrict__ tile_order) {
     __shared__ int wcnt[kWarpsPerCta][kBlocksPerTile];
     __shared__ int wpre[kWarpsPerCta][kBlocksPerTile];
-    const int tile = blockIdx.x;
+    // CTAs take the tiles longest list first (binning.cu tile_order_kernel); raster order without it
+    const int tile = tile_order ? tile_order[blockIdx.x] : blockIdx.x;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int2 range = ranges[tile];
     const int beg = range.x, list_end = range.y;
@@ -689,7 +691,7 @@ render_fwd_kernel(KParams kp, const float4* __restrict__ recs, const int2* __res
                   const int* __restrict__ stream_count, int* __restrict__ stream_used, int W, int H,
                   int tiles_x, float bg0, float bg1, float bg2, float* __restrict__ image,
                   float* __restrict__ t_final, int* __restrict__ processed, int* __restrict__ contributors,
-                  unsigned long long* __restrict__ counters) {
+                  unsigned long long* __restrict__ counters, const int* __restrict__ tile_order) {
     constexpr int kGroup = FwdGroup<FAM>::value;
     constexpr int kDepth = FwdStages<FAM>::value;  // stages of the bulk-copy ring
     __shared__ __align__(128) float4 ring[kFwdWarps][kDepth][kChunkVecs];
@@ -698,7 +700,8 @@ render_fwd_kernel(KParams kp, const float4* __restrict__ recs, const int2* __res
     // keeps the ring pointers and loop control in uniform registers
     const int lwarp = __reduce_min_sync(kFull, (int)(threadIdx.x >> 5)), lane = threadIdx.x & 31;
     const int gwarp = blockIdx.x * kFwdWarps + lwarp;
-    const int tile = gwarp / kBlocksPerTile, warp = gwarp % kBlocksPerTile;  // warp: the block inside the tile
+    const int warp = gwarp % kBlocksPerTile;  // the block inside the tile
+    const int tile = tile_order ? tile_order[gwarp / kBlocksPerTile] : gwarp / kBlocksPerTile;
     const int bx = (tile % tiles_x) * DARBS_TILE_SIZE + (warp & 1) * 8;
     const int by = (tile / tiles_x) * DARBS_TILE_SIZE + (warp >> 1) * 4;
     if (bx >= W || by >= H) return;  // whole block outside the image
@@ -1015,7 +1018,8 @@ render_bwd_kernel(KParams kp, const float4* __restrict__ recs, const int2* __res
                   const float4* __restrict__ streams, const int* __restrict__ stream_used, int W, int H,
                   int tiles_x, float bg0, float bg1, float bg2, const float* __restrict__ grad_image,
                   const float* __restrict__ t_final, const int* __restrict__ processed,
-                  float* __restrict__ grads, unsigned long long* __restrict__ counters) {
+                  float* __restrict__ grads, unsigned long long* __restrict__ counters,
+                  const int* __restrict__ tile_order) {
     __shared__ __align__(128) float4 ring[kBwdWarps][kBwdStages][kChunkVecs];
     __shared__ unsigned long long bars[kBwdWarps][kBwdStages];
     // [0]: wgt, then (y, z) pairs, or y alone for the Gaussian
@@ -1023,7 +1027,8 @@ render_bwd_kernel(KParams kp, const float4* __restrict__ recs, const int2* __res
     __shared__ float4 gpix[kBwdWarps][32];
     const int warp = __reduce_min_sync(kFull, (int)(threadIdx.x >> 5)), lane = threadIdx.x & 31;
     const int gwarp = blockIdx.x * kBwdWarps + warp;
-    const int tile = gwarp / kBlocksPerTile, blk = gwarp % kBlocksPerTile;  // blk: the forward's block index
+    const int blk = gwarp % kBlocksPerTile;  // the forward's block index
+    const int tile = tile_order ? tile_order[gwarp / kBlocksPerTile] : gwarp / kBlocksPerTile;
     const int bx = (tile % tiles_x) * DARBS_TILE_SIZE + (blk & 1) * 8;
     const int by = (tile / tiles_x) * DARBS_TILE_SIZE + (blk >> 1) * 4;
     if (bx >= W || by >= H) return;
@@ -1313,6 +1318,11 @@ darbs_status launch_pack(darbs_cuda_ctx* ctx, const KParams& kp, int64_t n, cons
 // so: a base depth per family, applied when the mean list is at least 1.5 times as long (the tail
 // path reads its entries from global memory and is slower per visit than the stream walk).
 // ctx->cull_segment > 0 overrides (darbs_cuda_set_cull_segment).
+// the CTA order of the render kernels: longest tile list first when this view's tile sort made one
+static const int* tile_order_ptr(const darbs_cuda_ctx* ctx) {
+    return ctx->tile_order_valid ? (const int*)ctx->tile_order.ptr : nullptr;
+}
+
 constexpr int kNoSegment = 1 << 30;
 int cull_segment(const darbs_cuda_ctx* ctx, const KParams& kp) {
     if (ctx->cull_segment > 0) return ctx->cull_segment;
@@ -1334,7 +1344,7 @@ darbs_status launch_cull(darbs_cuda_ctx* ctx, const KParams& kp) {
     cull_kernel<<<tiles, kThreads, 0, ctx->stream>>>(
         kp, (const float4*)ctx->recs.ptr, (const int2*)ctx->ranges.ptr, point_list_ptr(ctx), ctx->tiles_x,
         cull_segment(ctx, kp), (float4*)ctx->streams.ptr, (int*)ctx->stream_count.ptr,
-        (unsigned long long*)ctx->counters.ptr);
+        (unsigned long long*)ctx->counters.ptr, nullptr);  // raster order: neighbouring tiles share records
     return check_launch(ctx, "cull_kernel");
 }
 
@@ -1350,10 +1360,15 @@ darbs_status launch_render_fwd(darbs_cuda_ctx* ctx, const KParams& kp, int width
     const int* count = (const int*)ctx->stream_count.ptr;
     int* used = (int*)ctx->stream_count.ptr + (size_t)kBlocksPerTile * tiles;
     const int seg = cull_segment(ctx, kp);
+    if (ctx->tile_order_pending) {  // the ordering ran on the second stream, under the cull kernel
+        DARBS_CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->stream, ctx->order_ready, 0));
+        ctx->tile_order_pending = false;
+    }
 #define DARBS_LAUNCH_FWD_(F, T)                                                                      \
     render_fwd_kernel<F, T><<<tiles * (kBlocksPerTile / kFwdWarps), 32 * kFwdWarps, 0, ctx->stream>>>(  \
         kp, recs, ranges, plist, seg, (const float4*)ctx->streams.ptr, count, used, width, height,     \
-        ctx->tiles_x, bg[0], bg[1], bg[2], image, t_final, processed, contributors, counters)
+        ctx->tiles_x, bg[0], bg[1], bg[2], image, t_final, processed, contributors, counters,          \
+        tile_order_ptr(ctx))
 #define DARBS_LAUNCH_FWD(F)              \
     do {                                 \
         if (seg < kNoSegment)            \
@@ -1401,7 +1416,7 @@ darbs_status launch_render_bwd(darbs_cuda_ctx* ctx, const KParams& kp, int width
 #define DARBS_LAUNCH_BWD_(F, D)                                                                   \
     render_bwd_kernel<F, D><<<tiles * (kBlocksPerTile / kBwdWarps), kBwdThreads, 0, ctx->stream>>>(  \
         kp, recs, ranges, (const float4*)ctx->streams.ptr, used, width, height, ctx->tiles_x,     \
-        bg[0], bg[1], bg[2], grad_image, t_final, processed, sums, counters)
+        bg[0], bg[1], bg[2], grad_image, t_final, processed, sums, counters, tile_order_ptr(ctx))
 #define DARBS_LAUNCH_BWD(F)              \
     do {                                 \
         if (det)                         \
